@@ -1,0 +1,299 @@
+"""ORACLE — test infrastructure only.
+
+Plain, slow, obviously-correct fp64 CPU implementation of the ULTRA-HSTU layer
+(arXiv 2602.16986) hot path.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import it.  It shares
+no code with the CUDA path (``paper_2602_16986_b200``) and the CUDA path never
+imports it.  The seeded input generators live in ``paper_2602_16986_b200/synth.py``
+(no method arithmetic there) and are the only thing both sides use.
+
+Every function cites the passage it follows; PAPER.md = /root/reference/PAPER.md,
+``P:n`` = its line n; ``R<k>`` = reading k in DESIGN.md §3 (where the paper is
+silent or garbled).
+
+* layer_forward  — Eqs. 1-5 in Listing 1's order:
+      x^ = Norm(x); U,V,Q,K = SiLU(x^ W1 + b1); A = attention(Q,K,V);
+      Y = Norm(A) (.) U; out = Y W2 + b2 + x.
+* layer_backward — the exact chain rule of layer_forward; Listing 1
+  fixes the set of gradients returned (dx, d_norm_w, d_linear_w_1,
+  d_gated_norm_w, d_linear_w_2) and ``dx += dout``.
+* attention_forward / attention_backward — the C pair loops in attn_oracle.c
+  (Eq. 3; SLA mask P:140-146).
+* partition_lpt — the token-balanced partitioner: LPT on the cost model of
+  DESIGN.md §6; the load notion follows LBSL's
+  "load of a rank ... sum n_u^gamma".
+
+Matmuls are numpy (a library primitive used as one step); nothing is blocked,
+fused or reordered beyond the equations.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "attn_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "build", "libattn_oracle.so")
+_lib = None
+
+FULL = -1  # K1 < 0 selects full causal in the oracle
+
+
+def build(force: bool = False) -> str:
+    """Compile attn_oracle.c (plain C, -O2, OpenMP) into oracle/build/."""
+    os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        i64p = ctypes.POINTER(ctypes.c_int64)
+        dp = ctypes.POINTER(ctypes.c_double)
+        I64, D = ctypes.c_int64, ctypes.c_double
+        _lib.orc_mask_allows.argtypes = [I64, I64, I64, I64]
+        _lib.orc_mask_allows.restype = ctypes.c_int
+        _lib.orc_mask_nnz.argtypes = [I64, I64, I64]
+        _lib.orc_mask_nnz.restype = I64
+        _lib.orc_attn_fwd.argtypes = [ctypes.c_int, i32p, ctypes.c_int, ctypes.c_int,
+                                      dp, dp, dp, I64, I64, I64, D, D,
+                                      dp, I64, dp, I64, i64p, dp, I64, i64p]
+        _lib.orc_attn_fwd.restype = None
+        _lib.orc_attn_bwd.argtypes = [ctypes.c_int, i32p, ctypes.c_int, ctypes.c_int,
+                                      dp, dp, dp, I64, dp, I64, I64, I64, D, D,
+                                      dp, I64, dp, I64, i64p,
+                                      dp, dp, dp, I64, dp, dp, i64p]
+        _lib.orc_attn_bwd.restype = None
+        _lib.orc_num_threads.restype = ctypes.c_int
+    return _lib
+
+
+def num_threads() -> int:
+    return int(_load().orc_num_threads())
+
+
+def _ptr(a, ctype):
+    if a is None:
+        return None
+    return a.ctypes.data_as(ctypes.POINTER(ctype))
+
+
+def _f64(a):
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ----------------------------------------------------------------------------
+# mask (readings R1-R4)
+# ----------------------------------------------------------------------------
+def mask_allows(q: int, k: int, K1: int, K2: int) -> bool:
+    return bool(_load().orc_mask_allows(q, k, K1, K2))
+
+
+def mask_nnz(L: int, K1: int, K2: int) -> int:
+    """Allowed pairs of a length-L sequence, counted by enumeration."""
+    return int(_load().orc_mask_nnz(L, K1, K2))
+
+
+# ----------------------------------------------------------------------------
+# attention (Eq. 3) — C pair loops
+# ----------------------------------------------------------------------------
+@dataclass
+class AttnSpec:
+    """Mask + normalisation + rab of one layer (R1-R7)."""
+    K1: int = FULL              # window (inclusive); FULL (<0) = causal
+    K2: int = 0                 # global prefix tokens
+    alpha: float = 1.0          # score scale (R6)
+    N: float = 1.0              # silu(.)/N normaliser (R5)
+    pos_w: Optional[np.ndarray] = None   # [P]  (R7)
+    ts_w: Optional[np.ndarray] = None    # [NB] (R7)
+    timestamps: Optional[np.ndarray] = None  # int64 [T]
+
+
+def attention_forward(offsets, H, dh, q, k, v, spec: AttnSpec, return_work=False):
+    """A[r, h*dh:(h+1)*dh] for the jagged batch.  q,k,v: [T, >=H*dh] fp64."""
+    lib = _load()
+    offsets = np.ascontiguousarray(offsets, dtype=np.int32)
+    B = len(offsets) - 1
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    T = int(offsets[-1])
+    ld = q.shape[1]
+    assert k.shape[1] == ld and v.shape[1] == ld
+    A = np.zeros((T, H * dh), dtype=np.float64)
+    pos = _f64(spec.pos_w)
+    ts = _f64(spec.ts_w)
+    t = None
+    if ts is not None:
+        t = np.ascontiguousarray(spec.timestamps, dtype=np.int64)
+    work = ctypes.c_int64(0)
+    lib.orc_attn_fwd(B, _ptr(offsets, ctypes.c_int32), H, dh,
+                     _ptr(q, ctypes.c_double), _ptr(k, ctypes.c_double), _ptr(v, ctypes.c_double), ld,
+                     spec.K1, spec.K2, float(spec.alpha), float(spec.N),
+                     _ptr(pos, ctypes.c_double), 0 if pos is None else len(pos),
+                     _ptr(ts, ctypes.c_double), 0 if ts is None else len(ts),
+                     _ptr(t, ctypes.c_int64), _ptr(A, ctypes.c_double), H * dh, ctypes.byref(work))
+    return (A, int(work.value)) if return_work else A
+
+
+def attention_backward(offsets, H, dh, q, k, v, dA, spec: AttnSpec, return_work=False):
+    """(dQ, dK, dV, dpos, dts) — exact gradient of attention_forward."""
+    lib = _load()
+    offsets = np.ascontiguousarray(offsets, dtype=np.int32)
+    B = len(offsets) - 1
+    q, k, v, dA = _f64(q), _f64(k), _f64(v), _f64(dA)
+    T = int(offsets[-1])
+    ld = q.shape[1]
+    dQ = np.zeros((T, H * dh)); dK = np.zeros((T, H * dh)); dV = np.zeros((T, H * dh))
+    pos = _f64(spec.pos_w)
+    ts = _f64(spec.ts_w)
+    dpos = None if pos is None else np.zeros(len(pos))
+    dts = None if ts is None else np.zeros(len(ts))
+    t = None
+    if ts is not None:
+        t = np.ascontiguousarray(spec.timestamps, dtype=np.int64)
+    work = ctypes.c_int64(0)
+    lib.orc_attn_bwd(B, _ptr(offsets, ctypes.c_int32), H, dh,
+                     _ptr(q, ctypes.c_double), _ptr(k, ctypes.c_double), _ptr(v, ctypes.c_double), ld,
+                     _ptr(dA, ctypes.c_double), dA.shape[1],
+                     spec.K1, spec.K2, float(spec.alpha), float(spec.N),
+                     _ptr(pos, ctypes.c_double), 0 if pos is None else len(pos),
+                     _ptr(ts, ctypes.c_double), 0 if ts is None else len(ts),
+                     _ptr(t, ctypes.c_int64),
+                     _ptr(dQ, ctypes.c_double), _ptr(dK, ctypes.c_double), _ptr(dV, ctypes.c_double), H * dh,
+                     _ptr(dpos, ctypes.c_double), _ptr(dts, ctypes.c_double), ctypes.byref(work))
+    out = (dQ, dK, dV, dpos, dts)
+    return (out, int(work.value)) if return_work else out
+
+
+# ----------------------------------------------------------------------------
+# elementwise pieces (§3: "phi1 and phi2 are SiLU"; Eq. 1 / Eq. 4 Norm = LayerNorm, R9)
+# ----------------------------------------------------------------------------
+def silu(x):
+    return x / (1.0 + np.exp(-x))
+
+
+def silu_grad(x):
+    s = 1.0 / (1.0 + np.exp(-x))
+    return s * (1.0 + x * (1.0 - s))
+
+
+def layer_norm(x, w, b, eps):
+    """LayerNorm over the last dim, biased variance (R9).  Returns (y, mu, rstd)."""
+    mu = x.mean(axis=1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=1, keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    y = (x - mu) * rstd * w[None, :] + b[None, :]
+    return y, mu[:, 0], rstd[:, 0]
+
+
+def layer_norm_backward(g, x, mu, rstd, w):
+    """d/dx, d/dw, d/db of layer_norm for upstream gradient g."""
+    xt = (x - mu[:, None]) * rstd[:, None]
+    gh = g * w[None, :]
+    dx = rstd[:, None] * (gh - gh.mean(axis=1, keepdims=True)
+                          - xt * (gh * xt).mean(axis=1, keepdims=True))
+    return dx, (g * xt).sum(axis=0), g.sum(axis=0)
+
+
+# ----------------------------------------------------------------------------
+# the layer (Eqs. 1-5, Listing 1)
+# ----------------------------------------------------------------------------
+@dataclass
+class LayerParams:
+    ln1_w: np.ndarray
+    ln1_b: np.ndarray
+    w1: np.ndarray            # [d, 4d], columns U|V|Q|K (Listing 1 split order, R11)
+    ln2_w: np.ndarray
+    ln2_b: np.ndarray
+    w2: np.ndarray            # [d, d]
+    b1: Optional[np.ndarray] = None   # [4d]
+    b2: Optional[np.ndarray] = None   # [d]
+    eps: float = 1e-6
+
+
+def layer_forward(x, offsets, prm: LayerParams, H: int, spec: AttnSpec):
+    """Eqs. 1-5 in Listing 1's order.  Returns (out, cache)."""
+    x = _f64(x)
+    d = x.shape[1]
+    xh, mu1, rs1 = layer_norm(x, _f64(prm.ln1_w), _f64(prm.ln1_b), prm.eps)      # Eq. 1
+    h = xh @ _f64(prm.w1)                                                         # f1 (Eq. 2)
+    if prm.b1 is not None:
+        h = h + _f64(prm.b1)[None, :]
+    s = silu(h)                                                                   # phi1
+    U, V, Q, K = s[:, :d], s[:, d:2 * d], s[:, 2 * d:3 * d], s[:, 3 * d:]
+    A = attention_forward(offsets, H, d // H, Q, K, V, spec)                      # Eq. 3
+    Ah, mu2, rs2 = layer_norm(A, _f64(prm.ln2_w), _f64(prm.ln2_b), prm.eps)      # Norm(A)
+    Y = Ah * U                                                                    # (.) U, Eq. 4
+    out = Y @ _f64(prm.w2) + x                                                    # f2 + residual, Eqs. 4-5
+    if prm.b2 is not None:
+        out = out + _f64(prm.b2)[None, :]
+    cache = dict(x=x, xh=xh, mu1=mu1, rs1=rs1, h=h, U=U, V=V, Q=Q, K=K, A=A,
+                 Ah=Ah, mu2=mu2, rs2=rs2, Y=Y)
+    return out, cache
+
+
+def layer_backward(dout, offsets, prm: LayerParams, H: int, spec: AttnSpec, cache=None, x=None):
+    """Exact gradient of layer_forward for the loss sum(dout * out).
+
+    Returns (dx, grads) with grads keys ln1_w, ln1_b, w1, b1, ln2_w, ln2_b, w2, b2,
+    pos_w, ts_w.  Parameter gradients are sums over all tokens."""
+    if cache is None:
+        _, cache = layer_forward(x, offsets, prm, H, spec)
+    dout = _f64(dout)
+    d = dout.shape[1]
+    c = cache
+    g = {}
+    g["w2"] = c["Y"].T @ dout                                   # d_linear_w_2
+    g["b2"] = dout.sum(axis=0)
+    dY = dout @ _f64(prm.w2).T                                  # dy
+    dAh = dY * c["U"]                                           # gated_norm_backward
+    dU = dY * c["Ah"]
+    dA, g["ln2_w"], g["ln2_b"] = layer_norm_backward(dAh, c["A"], c["mu2"], c["rs2"], _f64(prm.ln2_w))
+    dQ, dK, dV, g["pos_w"], g["ts_w"] = attention_backward(      # attention_backward
+        offsets, H, d // H, c["Q"], c["K"], c["V"], dA, spec)
+    dS = np.concatenate([dU, dV, dQ, dK], axis=1)               # duqkv
+    dH = dS * silu_grad(c["h"])                                 # silu_backward
+    g["w1"] = c["xh"].T @ dH                                    # d_linear_w_1
+    g["b1"] = dH.sum(axis=0)
+    dxh = dH @ _f64(prm.w1).T                                   # d_normed_x
+    dx, g["ln1_w"], g["ln1_b"] = layer_norm_backward(dxh, c["x"], c["mu1"], c["rs1"], _f64(prm.ln1_w))
+    dx = dx + dout                                              # dx += dout
+    return dx, g
+
+
+# ----------------------------------------------------------------------------
+# token-balanced partitioner (load notion of P:112)
+# ----------------------------------------------------------------------------
+def seq_cost(L: int, d: int, H: int, K1: int, K2: int) -> float:
+    """c(L) = 3*(2 L d 4d + 2 L d d) + 14 d_h H nnz(L): fwd+bwd+remat GEMM flops plus
+    attention fwd (4 d_h) + bwd (10 d_h) flops per allowed pair."""
+    dh = d // H
+    return 3.0 * (2.0 * L * d * 4 * d + 2.0 * L * d * d) + 14.0 * dh * H * mask_nnz(L, K1, K2)
+
+
+def partition_lpt(lengths, world: int, d: int, H: int, K1: int, K2: int):
+    """Longest-processing-time-first: sort by (cost desc, seq id asc); give each
+    sequence to the least-loaded rank, lowest rank id on ties.  Step by step."""
+    costs = [seq_cost(int(L), d, H, K1, K2) for L in lengths]
+    order = sorted(range(len(lengths)), key=lambda i: (-costs[i], i))
+    load = [0.0] * world
+    owner = [-1] * len(lengths)
+    for i in order:
+        best = 0
+        for r in range(1, world):
+            if load[r] < load[best]:
+                best = r
+        owner[i] = best
+        load[best] += costs[i]
+    return owner, load
