@@ -1,0 +1,461 @@
+// norm.cu — HBM-bound row kernels of the layer: input LayerNorm (Eq. 1),
+// gated norm Y = Norm(A) (.) U (Eq. 4; "fused gated normalization kernel"
+// P:187) and their backward passes, the x^ rematerialisation from saved statistics
+// ("reusing saved layer-norm statistics"), column sums and the dQ finalise.
+//
+// One warp per row, 16-byte vector accesses (8 bf16 or 4 fp32 per access),
+// coalesced along the row; parameter-gradient partial sums are held in registers
+// across a grid-stride loop over rows and reduced once per block.
+#include <cuda_bf16.h>
+
+#include "internal.h"
+
+namespace uh {
+namespace {
+
+template <typename T> struct Vec;
+template <> struct Vec<float> {
+    static constexpr int N = 4;
+    __device__ __forceinline__ static void load(const float* p, float* v) {
+        float4 a = *reinterpret_cast<const float4*>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+    __device__ __forceinline__ static void store(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <> struct Vec<__nv_bfloat16> {
+    static constexpr int N = 8;
+    __device__ __forceinline__ static void load(const __nv_bfloat16* p, float* v) {
+        uint4 a = *reinterpret_cast<const uint4*>(p);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+    }
+    __device__ __forceinline__ static void store(__nv_bfloat16* p, const float* v) {
+        uint4 a;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&a);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        *reinterpret_cast<uint4*>(p) = a;
+    }
+};
+__device__ __forceinline__ void load4f(const float* p, float* v) { Vec<float>::load(p, v); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+constexpr int kRowsPerBlock = 8;  // 8 warps
+
+// ------------------------------------------------------------------ LN forward
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) ln_fwd_k(int64_t nrows, int d, const T* __restrict__ x, int64_t ldx,
+                                                const float* __restrict__ w, const float* __restrict__ b, float eps,
+                                                T* __restrict__ y, int64_t ldy, float* mean, float* rstd) {
+    constexpr int V = Vec<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    const int nch = d / V;
+    float v[CPL][V];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        int ch = lane + 32 * c;
+        if (ch < nch) {
+            Vec<T>::load(x + row * ldx + ch * V, v[c]);
+#pragma unroll
+            for (int e = 0; e < V; ++e) s += v[c][e];
+        }
+    }
+    const float mu = warp_sum(s) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+        if (lane + 32 * c < nch)
+#pragma unroll
+            for (int e = 0; e < V; ++e) { float t = v[c][e] - mu; q += t * t; }
+    const float rs = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        int ch = lane + 32 * c;
+        if (ch < nch) {
+            float wv[V], bv[V], o[V];
+#pragma unroll
+            for (int e = 0; e < V; e += 4) { load4f(w + ch * V + e, wv + e); load4f(b + ch * V + e, bv + e); }
+#pragma unroll
+            for (int e = 0; e < V; ++e) o[e] = (v[c][e] - mu) * rs * wv[e] + bv[e];
+            Vec<T>::store(y + row * ldy + ch * V, o);
+        }
+    }
+    if (lane == 0) {
+        if (mean) mean[row] = mu;
+        if (rstd) rstd[row] = rs;
+    }
+}
+
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) ln_apply_k(int64_t nrows, int d, const T* __restrict__ x, int64_t ldx,
+                                                  const float* __restrict__ w, const float* __restrict__ b,
+                                                  const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                  T* __restrict__ y, int64_t ldy) {
+    constexpr int V = Vec<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    const int nch = d / V;
+    const float mu = mean[row], rs = rstd[row];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        int ch = lane + 32 * c;
+        if (ch < nch) {
+            float v[V], wv[V], bv[V];
+            Vec<T>::load(x + row * ldx + ch * V, v);
+#pragma unroll
+            for (int e = 0; e < V; e += 4) { load4f(w + ch * V + e, wv + e); load4f(b + ch * V + e, bv + e); }
+#pragma unroll
+            for (int e = 0; e < V; ++e) v[e] = (v[e] - mu) * rs * wv[e] + bv[e];
+            Vec<T>::store(y + row * ldy + ch * V, v);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ gated norm forward
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) gated_fwd_k(int64_t nrows, int d, const T* __restrict__ A, int64_t lda,
+                                                   const T* __restrict__ U, int64_t ldu, const float* __restrict__ w,
+                                                   const float* __restrict__ b, float eps, T* __restrict__ Y,
+                                                   int64_t ldy, float* mean, float* rstd) {
+    constexpr int V = Vec<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    const int nch = d / V;
+    float v[CPL][V];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        int ch = lane + 32 * c;
+        if (ch < nch) {
+            Vec<T>::load(A + row * lda + ch * V, v[c]);
+#pragma unroll
+            for (int e = 0; e < V; ++e) s += v[c][e];
+        }
+    }
+    const float mu = warp_sum(s) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+        if (lane + 32 * c < nch)
+#pragma unroll
+            for (int e = 0; e < V; ++e) { float t = v[c][e] - mu; q += t * t; }
+    const float rs = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        int ch = lane + 32 * c;
+        if (ch < nch) {
+            float wv[V], bv[V], u[V], o[V];
+            Vec<T>::load(U + row * ldu + ch * V, u);
+#pragma unroll
+            for (int e = 0; e < V; e += 4) { load4f(w + ch * V + e, wv + e); load4f(b + ch * V + e, bv + e); }
+#pragma unroll
+            for (int e = 0; e < V; ++e) o[e] = ((v[c][e] - mu) * rs * wv[e] + bv[e]) * u[e];
+            Vec<T>::store(Y + row * ldy + ch * V, o);
+        }
+    }
+    if (lane == 0) {
+        if (mean) mean[row] = mu;
+        if (rstd) rstd[row] = rs;
+    }
+}
+
+// block-level reduction of per-lane parameter-gradient partials, then one atomic per column
+template <typename T, int CPL>
+__device__ __forceinline__ void flush_param_grads(int d, float (*pw)[Vec<T>::N], float (*pb)[Vec<T>::N], float* dw,
+                                                  float* db, float* red /* smem [2][d] */) {
+    constexpr int V = Vec<T>::N;
+    const int lane = threadIdx.x & 31;
+    const int nch = d / V;
+    for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) red[i] = 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        int ch = lane + 32 * c;
+        if (ch < nch)
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                atomicAdd(&red[ch * V + e], pw[c][e]);
+                atomicAdd(&red[d + ch * V + e], pb[c][e]);
+            }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        if (dw) atomicAdd(dw + i, red[i]);
+        if (db) atomicAdd(db + i, red[d + i]);
+    }
+}
+
+// ------------------------------------------------------------------ gated norm backward
+// Given dY: A^ = (A - mu) rstd w + b, Y = A^ U;  dA^ = dY U, dU = dY A^ -> dH_U = dU * G_U;
+// dA = rstd (g - mean(g) - x~ mean(g x~)), g = dA^ w;  dw += dA^ x~, db += dA^.
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) gated_bwd_k(int64_t nrows, int d, const T* __restrict__ dY, int64_t lddy,
+                                                   const T* __restrict__ A, int64_t lda, const T* __restrict__ U,
+                                                   int64_t ldu, const T* __restrict__ GU, int64_t ldg,
+                                                   const float* __restrict__ w, const float* __restrict__ b,
+                                                   const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                   T* __restrict__ dA, int64_t ldda, T* __restrict__ dHU, int64_t ldh,
+                                                   T* __restrict__ Y, int64_t ldy, float* dw, float* db) {
+    constexpr int V = Vec<T>::N;
+    extern __shared__ float red[];
+    const int lane = threadIdx.x & 31;
+    const int nch = d / V;
+    float pw[CPL][V], pb[CPL][V];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+        for (int e = 0; e < V; ++e) { pw[c][e] = 0.f; pb[c][e] = 0.f; }
+    for (int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5); row < nrows;
+         row += (int64_t)gridDim.x * kRowsPerBlock) {
+        const float mu = mean[row], rs = rstd[row];
+        float xt[CPL][V], g[CPL][V];
+        float sg = 0.f, sgx = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            int ch = lane + 32 * c;
+            if (ch < nch) {
+                float a[V], u[V], dy[V], gu[V], wv[V], bv[V], y[V], dh[V];
+                Vec<T>::load(A + row * lda + ch * V, a);
+                Vec<T>::load(U + row * ldu + ch * V, u);
+                Vec<T>::load(dY + row * lddy + ch * V, dy);
+                Vec<T>::load(GU + row * ldg + ch * V, gu);
+#pragma unroll
+                for (int e = 0; e < V; e += 4) { load4f(w + ch * V + e, wv + e); load4f(b + ch * V + e, bv + e); }
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    xt[c][e] = (a[e] - mu) * rs;
+                    float ah = xt[c][e] * wv[e] + bv[e];
+                    y[e] = ah * u[e];
+                    float dah = dy[e] * u[e];
+                    dh[e] = dy[e] * ah * gu[e];
+                    g[c][e] = dah * wv[e];
+                    pw[c][e] += dah * xt[c][e];
+                    pb[c][e] += dah;
+                    sg += g[c][e];
+                    sgx += g[c][e] * xt[c][e];
+                }
+                if (Y) Vec<T>::store(Y + row * ldy + ch * V, y);
+                Vec<T>::store(dHU + row * ldh + ch * V, dh);
+            }
+        }
+        const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            int ch = lane + 32 * c;
+            if (ch < nch) {
+                float o[V];
+#pragma unroll
+                for (int e = 0; e < V; ++e) o[e] = rs * (g[c][e] - mg - xt[c][e] * mgx);
+                Vec<T>::store(dA + row * ldda + ch * V, o);
+            }
+        }
+    }
+    flush_param_grads<T, CPL>(d, pw, pb, dw, db, red);
+}
+
+// ------------------------------------------------------------------ LN backward (+ residual)
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* __restrict__ dxh, int64_t ldg,
+                                                const T* __restrict__ x, int64_t ldx, const float* __restrict__ w,
+                                                const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                const T* __restrict__ dres, int64_t ldr, T* __restrict__ dx,
+                                                int64_t lddx, float* dw, float* db) {
+    constexpr int V = Vec<T>::N;
+    extern __shared__ float red[];
+    const int lane = threadIdx.x & 31;
+    const int nch = d / V;
+    float pw[CPL][V], pb[CPL][V];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+#pragma unroll
+        for (int e = 0; e < V; ++e) { pw[c][e] = 0.f; pb[c][e] = 0.f; }
+    for (int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5); row < nrows;
+         row += (int64_t)gridDim.x * kRowsPerBlock) {
+        const float mu = mean[row], rs = rstd[row];
+        float xt[CPL][V], g[CPL][V];
+        float sg = 0.f, sgx = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            int ch = lane + 32 * c;
+            if (ch < nch) {
+                float xv[V], gv[V], wv[V];
+                Vec<T>::load(x + row * ldx + ch * V, xv);
+                Vec<T>::load(dxh + row * ldg + ch * V, gv);
+#pragma unroll
+                for (int e = 0; e < V; e += 4) load4f(w + ch * V + e, wv + e);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    xt[c][e] = (xv[e] - mu) * rs;
+                    g[c][e] = gv[e] * wv[e];
+                    pw[c][e] += gv[e] * xt[c][e];
+                    pb[c][e] += gv[e];
+                    sg += g[c][e];
+                    sgx += g[c][e] * xt[c][e];
+                }
+            }
+        }
+        const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            int ch = lane + 32 * c;
+            if (ch < nch) {
+                float o[V], r[V];
+                if (dres) Vec<T>::load(dres + row * ldr + ch * V, r);
+#pragma unroll
+                for (int e = 0; e < V; ++e) o[e] = rs * (g[c][e] - mg - xt[c][e] * mgx) + (dres ? r[e] : 0.f);
+                Vec<T>::store(dx + row * lddx + ch * V, o);
+            }
+        }
+    }
+    flush_param_grads<T, CPL>(d, pw, pb, dw, db, red);
+}
+
+// ------------------------------------------------------------------ column sums / scale
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_k(int64_t nrows, int n, const T* __restrict__ M, int64_t ldm,
+                                                int64_t rows_per_block, float* out) {
+    const int col = blockIdx.x * 256 + threadIdx.x;
+    if (col >= n) return;
+    const int64_t r0 = blockIdx.y * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
+    float s = 0.f;
+    for (int64_t r = r0; r < r1; ++r) s += static_cast<float>(M[r * ldm + col]);
+    atomicAdd(out + col, s);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) scale_store_k(int64_t nrows, int n, const float* __restrict__ acc, int64_t lda,
+                                                     const T* __restrict__ G, int64_t ldg, T* __restrict__ dst,
+                                                     int64_t ldd) {
+    constexpr int V = Vec<T>::N;
+    const int nch = n / V;
+    const int64_t total = nrows * nch;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / nch;
+        const int ch = (int)(i - r * nch);
+        float a[V], gv[V];
+#pragma unroll
+        for (int e = 0; e < V; e += 4) load4f(acc + r * lda + ch * V + e, a + e);
+        Vec<T>::load(G + r * ldg + ch * V, gv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) a[e] *= gv[e];
+        Vec<T>::store(dst + r * ldd + ch * V, a);
+    }
+}
+
+template <typename T>
+int cpl_for(int d) { return (d / Vec<T>::N + 31) / 32; }
+
+int grid_rows(int64_t T) { return (int)((T + kRowsPerBlock - 1) / kRowsPerBlock); }
+int grid_persistent(int64_t T) {
+    int64_t want = (T + kRowsPerBlock - 1) / kRowsPerBlock;
+    int64_t cap = 4LL * num_sms();
+    return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+
+// CPL dispatch: chunks-per-lane in {1,2,4,8} covers d up to 1024 (bf16) / 1024 (fp32)
+#define UH_CPL_DISPATCH(T, d, ...)                                              \
+    do {                                                                        \
+        int cpl_ = cpl_for<T>(d);                                               \
+        if (cpl_ <= 1) { constexpr int CPL = 1; __VA_ARGS__; }                  \
+        else if (cpl_ <= 2) { constexpr int CPL = 2; __VA_ARGS__; }             \
+        else if (cpl_ <= 4) { constexpr int CPL = 4; __VA_ARGS__; }             \
+        else if (cpl_ <= 8) { constexpr int CPL = 8; __VA_ARGS__; }             \
+        else return fail(UH_ERR_UNSUPPORTED, "model dim too large for norm kernels"); \
+    } while (0)
+
+#define UH_DT_DISPATCH(dt, ...)                                    \
+    do {                                                           \
+        if ((dt) == UH_BF16) { using T = __nv_bfloat16; __VA_ARGS__; } \
+        else { using T = float; __VA_ARGS__; }                     \
+    } while (0)
+
+uh_status ln_fwd(uh_dtype dt, int64_t T_, int d, const void* x, int64_t ldx, const float* w, const float* b, float eps,
+                 void* y, int64_t ldy, float* mean, float* rstd, cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
+        ln_fwd_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)x, ldx, w, b, eps, (T*)y, ldy, mean, rstd)));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status ln_apply(uh_dtype dt, int64_t T_, int d, const void* x, int64_t ldx, const float* w, const float* b,
+                   const float* mean, const float* rstd, void* y, int64_t ldy, cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
+        ln_apply_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)x, ldx, w, b, mean, rstd, (T*)y, ldy)));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status gated_norm_fwd(uh_dtype dt, int64_t T_, int d, const void* A, int64_t lda, const void* U, int64_t ldu,
+                         const float* w, const float* b, float eps, void* Y, int64_t ldy, float* mean, float* rstd,
+                         cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
+        gated_fwd_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)A, lda, (const T*)U, ldu, w, b, eps,
+                                                           (T*)Y, ldy, mean, rstd)));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status gated_norm_bwd(uh_dtype dt, int64_t T_, int d, const void* dY, int64_t lddy, const void* A, int64_t lda,
+                         const void* U, int64_t ldu, const void* GU, int64_t ldg, const float* w, const float* b,
+                         const float* mean, const float* rstd, void* dA, int64_t ldda, void* dHU, int64_t ldh,
+                         void* Y, int64_t ldy, float* dw, float* db, cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
+        gated_bwd_k<T, CPL><<<grid_persistent(T_), 256, 2 * d * sizeof(float), st>>>(
+            T_, d, (const T*)dY, lddy, (const T*)A, lda, (const T*)U, ldu, (const T*)GU, ldg, w, b, mean, rstd,
+            (T*)dA, ldda, (T*)dHU, ldh, (T*)Y, ldy, dw, db)));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status ln_bwd(uh_dtype dt, int64_t T_, int d, const void* dxh, int64_t ldg, const void* x, int64_t ldx,
+                 const float* w, const float* mean, const float* rstd, const void* dres, int64_t ldr, void* dx,
+                 int64_t lddx, float* dw, float* db, cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
+        ln_bwd_k<T, CPL><<<grid_persistent(T_), 256, 2 * d * sizeof(float), st>>>(
+            T_, d, (const T*)dxh, ldg, (const T*)x, ldx, w, mean, rstd, (const T*)dres, ldr, (T*)dx, lddx, dw, db)));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status colsum(uh_dtype dt, int64_t T_, int n, const void* M, int64_t ldm, float* out, cudaStream_t st) {
+    if (T_ == 0 || n == 0) return UH_OK;
+    const int64_t cols_blocks = (n + 255) / 256;
+    int64_t ry = (2 * num_sms() + cols_blocks - 1) / cols_blocks;
+    int64_t rpb = (T_ + ry - 1) / ry;
+    if (rpb < 64) rpb = 64;
+    ry = (T_ + rpb - 1) / rpb;
+    dim3 grid((unsigned)cols_blocks, (unsigned)ry);
+    UH_DT_DISPATCH(dt, colsum_k<T><<<grid, 256, 0, st>>>(T_, n, (const T*)M, ldm, rpb, out));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status scale_store(uh_dtype dt, int64_t T_, int n, const float* acc, int64_t lda, const void* G, int64_t ldg,
+                      void* dst, int64_t ldd, cudaStream_t st) {
+    if (T_ == 0 || n == 0) return UH_OK;
+    UH_DT_DISPATCH(dt, scale_store_k<T><<<4 * num_sms(), 256, 0, st>>>(T_, n, acc, lda, (const T*)G, ldg, (T*)dst, ldd));
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+}  // namespace uh

@@ -1,0 +1,382 @@
+"""Thin ctypes binding of libuhstu (include/uhstu.h).
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA
+kernels.  PyTorch provides device memory and the current stream.  If the shared
+library is missing this module raises on first use — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libuhstu.so")
+WINDOW_FULL = 2**31 - 1
+
+BF16, F32 = 0, 1
+_DT = {torch.bfloat16: BF16, torch.float32: F32}
+
+_lib = None
+
+
+class UhError(RuntimeError):
+    def __init__(self, status: int, name: str, detail: str):
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+        self.name = name
+
+
+# ----------------------------------------------------------------------------- structs
+class Jagged(ctypes.Structure):
+    _fields_ = [("num_seqs", ctypes.c_int32), ("max_len", ctypes.c_int32), ("total_tokens", ctypes.c_int64),
+                ("offsets", ctypes.c_void_p), ("host_offsets", ctypes.POINTER(ctypes.c_int32))]
+
+
+class Mask(ctypes.Structure):
+    _fields_ = [("window", ctypes.c_int32), ("n_global", ctypes.c_int32)]
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [("num_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("alpha", ctypes.c_float),
+                ("norm_n", ctypes.c_float), ("pos_bias", ctypes.c_void_p), ("pos_bias_len", ctypes.c_int32),
+                ("time_bias", ctypes.c_void_p), ("time_bias_len", ctypes.c_int32), ("timestamps", ctypes.c_void_p)]
+
+
+class LayerParams(ctypes.Structure):
+    _fields_ = [("ln1_w", ctypes.c_void_p), ("ln1_b", ctypes.c_void_p), ("w1", ctypes.c_void_p),
+                ("b1", ctypes.c_void_p), ("ln2_w", ctypes.c_void_p), ("ln2_b", ctypes.c_void_p),
+                ("w2", ctypes.c_void_p), ("b2", ctypes.c_void_p), ("attn", AttnDesc), ("eps", ctypes.c_float)]
+
+
+class LayerSaved(ctypes.Structure):
+    _fields_ = [("attn", ctypes.c_void_p), ("ln1_mean", ctypes.c_void_p), ("ln1_rstd", ctypes.c_void_p),
+                ("ln2_mean", ctypes.c_void_p), ("ln2_rstd", ctypes.c_void_p)]
+
+
+class LayerGrads(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("ln1_w", "ln1_b", "w1", "b1", "ln2_w", "ln2_b", "w2", "b2", "pos_bias", "time_bias")]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libuhstu not built ({LIB_PATH} missing): run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        L.uh_status_string.restype = ctypes.c_char_p
+        L.uh_status_string.argtypes = [ctypes.c_int]
+        L.uh_last_error.restype = ctypes.c_char_p
+        L.uh_abi_version.restype = ctypes.c_int
+        L.uh_mask_nnz.restype = i64
+        L.uh_mask_nnz.argtypes = [Mask, i64]
+        L.uh_batch_nnz.restype = i64
+        L.uh_batch_nnz.argtypes = [P(Jagged), Mask]
+        L.uh_attn_workspace_bytes.argtypes = [P(Jagged), Mask, P(AttnDesc), ctypes.c_int, ctypes.c_int, P(sz)]
+        L.uh_attn_fwd.argtypes = [P(Jagged), Mask, P(AttnDesc), ctypes.c_int, vp, vp, vp, i64, vp, i64, vp, sz, vp]
+        L.uh_attn_bwd.argtypes = [P(Jagged), Mask, P(AttnDesc), ctypes.c_int, vp, vp, vp, i64, vp, i64,
+                                  vp, vp, vp, i64, vp, vp, vp, sz, vp]
+        L.uh_layer_workspace_bytes.argtypes = [P(Jagged), Mask, P(LayerParams), ctypes.c_int, ctypes.c_int, P(sz)]
+        L.uh_layer_fwd.argtypes = [P(Jagged), Mask, P(LayerParams), ctypes.c_int, vp, vp, P(LayerSaved), vp, sz, vp]
+        L.uh_layer_bwd.argtypes = [P(Jagged), Mask, P(LayerParams), ctypes.c_int, vp, P(LayerSaved), vp, vp,
+                                   P(LayerGrads), ctypes.c_int, vp, sz, vp]
+        L.uh_jagged_gather.argtypes = [P(Jagged), P(i32), i32, vp, i64, i64, i32, vp, P(i32), vp, vp]
+        L.uh_jagged_slice_latest.argtypes = [P(Jagged), i32, vp, i64, i64, i32, vp, P(i32), vp, vp]
+        L.uh_jagged_to_padded.argtypes = [P(Jagged), vp, i64, i32, i32, vp, vp]
+        L.uh_padded_to_jagged.argtypes = [P(Jagged), vp, i64, i32, i32, vp, vp]
+        L.uh_partition_lpt.argtypes = [P(i32), i32, i32, Mask, i32, i32, P(i32), P(ctypes.c_double)]
+        for f in ("uh_attn_workspace_bytes", "uh_attn_fwd", "uh_attn_bwd", "uh_layer_workspace_bytes",
+                  "uh_layer_fwd", "uh_layer_bwd", "uh_jagged_gather", "uh_jagged_slice_latest",
+                  "uh_jagged_to_padded", "uh_padded_to_jagged", "uh_partition_lpt"):
+            getattr(L, f).restype = ctypes.c_int
+        L.uh_test_gemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, i64, ctypes.c_int, vp, i64,
+                                   ctypes.c_int, ctypes.c_int, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp]
+        L.uh_test_gemm.restype = ctypes.c_int
+        if L.uh_abi_version() != 1:
+            raise RuntimeError("libuhstu ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list:
+    return ["uh_status_string", "uh_last_error", "uh_abi_version", "uh_mask_nnz", "uh_batch_nnz",
+            "uh_attn_workspace_bytes", "uh_attn_fwd", "uh_attn_bwd", "uh_layer_workspace_bytes", "uh_layer_fwd",
+            "uh_layer_bwd", "uh_jagged_gather", "uh_jagged_slice_latest", "uh_jagged_to_padded",
+            "uh_padded_to_jagged", "uh_partition_lpt"]
+
+
+def _check(st: int):
+    if st != 0:
+        L = lib()
+        raise UhError(st, L.uh_status_string(st).decode(), L.uh_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+# ----------------------------------------------------------------------------- jagged batch
+class JaggedBatch:
+    """Host + device copies of the offsets of a jagged batch."""
+
+    def __init__(self, offsets, device="cuda"):
+        off = np.ascontiguousarray(np.asarray(offsets, dtype=np.int32))
+        self.host = off
+        self.lengths = np.diff(off)
+        self.B = len(off) - 1
+        self.T = int(off[-1]) if len(off) else 0
+        self.max_len = int(self.lengths.max()) if self.B > 0 else 0
+        self.dev = torch.from_numpy(off.copy()).to(device) if device is not None else None
+        self.c = Jagged(self.B, self.max_len, self.T,
+                        ctypes.c_void_p(self.dev.data_ptr()) if self.dev is not None else None,
+                        self.host.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+
+    @staticmethod
+    def from_lengths(lengths, device="cuda"):
+        off = np.zeros(len(lengths) + 1, np.int32)
+        off[1:] = np.cumsum(lengths)
+        return JaggedBatch(off, device)
+
+
+def mask(window: int = WINDOW_FULL, n_global: int = 0) -> Mask:
+    return Mask(int(min(window, WINDOW_FULL)), int(n_global))
+
+
+@dataclass
+class Attn:
+    """Attention descriptor (uh_attn_desc) with the tensors it points to kept alive."""
+    num_heads: int
+    head_dim: int
+    alpha: float = 1.0
+    norm_n: float = 1.0
+    pos_bias: Optional[torch.Tensor] = None      # fp32 [P]
+    time_bias: Optional[torch.Tensor] = None     # fp32 [NB]
+    timestamps: Optional[torch.Tensor] = None    # int64 [T]
+
+    def c(self) -> AttnDesc:
+        return AttnDesc(self.num_heads, self.head_dim, self.alpha, self.norm_n,
+                        _ptr(self.pos_bias), 0 if self.pos_bias is None else self.pos_bias.numel(),
+                        _ptr(self.time_bias), 0 if self.time_bias is None else self.time_bias.numel(),
+                        _ptr(self.timestamps))
+
+
+def mask_nnz(m: Mask, L: int) -> int:
+    return int(lib().uh_mask_nnz(m, L))
+
+
+def batch_nnz(jag: JaggedBatch, m: Mask) -> int:
+    return int(lib().uh_batch_nnz(ctypes.byref(jag.c), m))
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {t.dtype}")
+    return _DT[t.dtype]
+
+
+# ----------------------------------------------------------------------------- attention
+def attn_workspace_bytes(jag, m, desc: Attn, dtype: int, backward: bool) -> int:
+    n = ctypes.c_size_t(0)
+    d = desc.c()
+    _check(lib().uh_attn_workspace_bytes(ctypes.byref(jag.c), m, ctypes.byref(d), dtype, int(backward), ctypes.byref(n)))
+    return int(n.value)
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def attn_fwd(jag: JaggedBatch, m: Mask, desc: Attn, q, k, v, out=None, ws=None):
+    """A = attention(Q, K, V) for the jagged batch; q/k/v may be column views of one buffer."""
+    dt = _dtype_code(q)
+    width = desc.num_heads * desc.head_dim
+    if out is None:
+        out = torch.empty(q.shape[0], width, dtype=q.dtype, device=q.device)
+    d = desc.c()
+    if ws is None:
+        ws = _ws(attn_workspace_bytes(jag, m, desc, dt, False), q.device)
+    _check(lib().uh_attn_fwd(ctypes.byref(jag.c), m, ctypes.byref(d), dt, _ptr(q), _ptr(k), _ptr(v), q.stride(0),
+                             _ptr(out), out.stride(0), _ptr(ws), ws.numel(), _stream()))
+    return out
+
+
+def attn_bwd(jag: JaggedBatch, m: Mask, desc: Attn, q, k, v, dout, dq=None, dk=None, dv=None,
+             dpos=None, dts=None, ws=None):
+    """(dQ, dK, dV, dpos, dts); dpos/dts are fp32 and accumulated into if given."""
+    dt = _dtype_code(q)
+    width = desc.num_heads * desc.head_dim
+    mk = lambda: torch.empty(q.shape[0], width, dtype=q.dtype, device=q.device)
+    if dq is None and dk is None and dv is None:
+        g = torch.empty(q.shape[0], 3 * width, dtype=q.dtype, device=q.device)
+        dq, dk, dv = g[:, :width], g[:, width:2 * width], g[:, 2 * width:]
+    dq = mk() if dq is None else dq
+    dk = mk() if dk is None else dk
+    dv = mk() if dv is None else dv
+    if dpos is None and desc.pos_bias is not None:
+        dpos = torch.zeros_like(desc.pos_bias)
+    if dts is None and desc.time_bias is not None:
+        dts = torch.zeros_like(desc.time_bias)
+    assert dq.stride(0) == dk.stride(0) == dv.stride(0)
+    d = desc.c()
+    if ws is None:
+        ws = _ws(attn_workspace_bytes(jag, m, desc, dt, True), q.device)
+    _check(lib().uh_attn_bwd(ctypes.byref(jag.c), m, ctypes.byref(d), dt, _ptr(q), _ptr(k), _ptr(v), q.stride(0),
+                             _ptr(dout), dout.stride(0), _ptr(dq), _ptr(dk), _ptr(dv), dq.stride(0),
+                             _ptr(dpos), _ptr(dts), _ptr(ws), ws.numel(), _stream()))
+    return dq, dk, dv, dpos, dts
+
+
+# ----------------------------------------------------------------------------- layer
+@dataclass
+class Params:
+    """One HSTU layer's parameters (Listing 1 signature): LN1, W1 [d,4d] (+b1), LN2, W2 [d,d] (+b2)."""
+    ln1_w: torch.Tensor
+    ln1_b: torch.Tensor
+    w1: torch.Tensor
+    ln2_w: torch.Tensor
+    ln2_b: torch.Tensor
+    w2: torch.Tensor
+    b1: Optional[torch.Tensor] = None
+    b2: Optional[torch.Tensor] = None
+    eps: float = 1e-6
+
+    def c(self, attn: Attn) -> LayerParams:
+        return LayerParams(_ptr(self.ln1_w), _ptr(self.ln1_b), _ptr(self.w1), _ptr(self.b1), _ptr(self.ln2_w),
+                           _ptr(self.ln2_b), _ptr(self.w2), _ptr(self.b2), attn.c(), self.eps)
+
+
+@dataclass
+class Saved:
+    attn: torch.Tensor
+    ln1_mean: torch.Tensor
+    ln1_rstd: torch.Tensor
+    ln2_mean: torch.Tensor
+    ln2_rstd: torch.Tensor
+
+    def c(self) -> LayerSaved:
+        return LayerSaved(_ptr(self.attn), _ptr(self.ln1_mean), _ptr(self.ln1_rstd), _ptr(self.ln2_mean),
+                          _ptr(self.ln2_rstd))
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in (self.attn, self.ln1_mean, self.ln1_rstd,
+                                                          self.ln2_mean, self.ln2_rstd))
+
+
+def layer_workspace_bytes(jag, m, prm: Params, attn: Attn, dtype: int, backward: bool) -> int:
+    n = ctypes.c_size_t(0)
+    p = prm.c(attn)
+    _check(lib().uh_layer_workspace_bytes(ctypes.byref(jag.c), m, ctypes.byref(p), dtype, int(backward),
+                                          ctypes.byref(n)))
+    return int(n.value)
+
+
+def layer_fwd(jag, m, prm: Params, attn: Attn, x, save: bool = True, out=None, ws=None):
+    dt = _dtype_code(x)
+    T, d = x.shape
+    out = torch.empty_like(x) if out is None else out
+    saved = None
+    if save:
+        f = lambda: torch.empty(T, dtype=torch.float32, device=x.device)
+        saved = Saved(torch.empty_like(x), f(), f(), f(), f())
+    p = prm.c(attn)
+    if ws is None:
+        ws = _ws(layer_workspace_bytes(jag, m, prm, attn, dt, False), x.device)
+    sc = saved.c() if saved is not None else None
+    _check(lib().uh_layer_fwd(ctypes.byref(jag.c), m, ctypes.byref(p), dt, _ptr(x), _ptr(out),
+                              ctypes.byref(sc) if sc is not None else None, _ptr(ws), ws.numel(), _stream()))
+    return out, saved
+
+
+def layer_bwd(jag, m, prm: Params, attn: Attn, x, saved: Saved, dout, grads: Optional[dict] = None,
+              accumulate: bool = False, dx=None, ws=None):
+    """Returns (dx, grads) — grads: fp32 tensors keyed like Params (+ pos_bias, time_bias)."""
+    dt = _dtype_code(x)
+    dx = torch.empty_like(x) if dx is None else dx
+    if grads is None:
+        z = lambda t: None if t is None else torch.zeros(t.shape, dtype=torch.float32, device=x.device)
+        grads = dict(ln1_w=z(prm.ln1_w), ln1_b=z(prm.ln1_b), w1=z(prm.w1), b1=z(prm.b1), ln2_w=z(prm.ln2_w),
+                     ln2_b=z(prm.ln2_b), w2=z(prm.w2), b2=z(prm.b2), pos_bias=z(attn.pos_bias),
+                     time_bias=z(attn.time_bias))
+    g = LayerGrads(*[_ptr(grads.get(n)) for n, _ in LayerGrads._fields_])
+    p = prm.c(attn)
+    sc = saved.c()
+    if ws is None:
+        ws = _ws(layer_workspace_bytes(jag, m, prm, attn, dt, True), x.device)
+    _check(lib().uh_layer_bwd(ctypes.byref(jag.c), m, ctypes.byref(p), dt, _ptr(x), ctypes.byref(sc), _ptr(dout),
+                              _ptr(dx), ctypes.byref(g), int(accumulate), _ptr(ws), ws.numel(), _stream()))
+    return dx, grads
+
+
+# ----------------------------------------------------------------------------- jagged ops
+def _offsets_out(n: int):
+    return np.zeros(n + 1, np.int32)
+
+
+def jagged_gather(jag: JaggedBatch, seq_ids: Sequence[int], x: torch.Tensor):
+    ids = np.ascontiguousarray(np.asarray(seq_ids, np.int32))
+    n = len(ids)
+    tot = int(sum(jag.lengths[i] for i in ids))
+    y = torch.empty(tot, x.shape[1], dtype=x.dtype, device=x.device)
+    off = _offsets_out(n)
+    _check(lib().uh_jagged_gather(ctypes.byref(jag.c), ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n,
+                                  _ptr(x), x.stride(0), x.shape[1], x.element_size(), _ptr(y),
+                                  off.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), None, _stream()))
+    return y, JaggedBatch(off, x.device)
+
+
+def jagged_slice_latest(jag: JaggedBatch, l_keep: int, x: torch.Tensor):
+    tot = int(np.minimum(jag.lengths, l_keep).sum())
+    y = torch.empty(tot, x.shape[1], dtype=x.dtype, device=x.device)
+    off = _offsets_out(jag.B)
+    _check(lib().uh_jagged_slice_latest(ctypes.byref(jag.c), int(l_keep), _ptr(x), x.stride(0), x.shape[1],
+                                        x.element_size(), _ptr(y), off.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                        None, _stream()))
+    return y, JaggedBatch(off, x.device)
+
+
+def jagged_to_padded(jag: JaggedBatch, x: torch.Tensor, max_len: int):
+    y = torch.empty(jag.B, max_len, x.shape[1], dtype=x.dtype, device=x.device)
+    _check(lib().uh_jagged_to_padded(ctypes.byref(jag.c), _ptr(x), x.shape[1], x.element_size(), max_len, _ptr(y),
+                                     _stream()))
+    return y
+
+
+def padded_to_jagged(jag: JaggedBatch, y: torch.Tensor):
+    x = torch.empty(jag.T, y.shape[2], dtype=y.dtype, device=y.device)
+    _check(lib().uh_padded_to_jagged(ctypes.byref(jag.c), _ptr(y), y.shape[2], y.element_size(), y.shape[1], _ptr(x),
+                                     _stream()))
+    return x
+
+
+def test_gemm(A, B, a_mn: bool, b_mn: bool, epi: int, M: int, N: int, K: int, bias=None, resid=None,
+              out0=None, out1=None):
+    """Test hook (include/uhstu_testing.h): the internal projection GEMM."""
+    dt = _dtype_code(A)
+    if out0 is None:
+        out0 = torch.zeros(M, N, dtype=torch.float32 if epi == 2 else A.dtype, device=A.device)
+    _check(lib().uh_test_gemm(M, N, K, _ptr(A), A.stride(0), int(a_mn), _ptr(B), B.stride(0), int(b_mn), epi,
+                              _ptr(out0), out0.stride(0), _ptr(out1), 0 if out1 is None else out1.stride(0),
+                              _ptr(bias), _ptr(resid), 0 if resid is None else resid.stride(0), dt, _stream()))
+    return out0, out1
+
+
+# ----------------------------------------------------------------------------- partitioner
+def partition_lpt(lengths, world: int, m: Mask, d: int, num_heads: int):
+    L = np.ascontiguousarray(np.asarray(lengths, np.int32))
+    owner = np.zeros(len(L), np.int32)
+    cost = np.zeros(world, np.float64)
+    _check(lib().uh_partition_lpt(L.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(L), world, m, d, num_heads,
+                                  owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                  cost.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return owner, cost

@@ -1,0 +1,127 @@
+"""Host-side tests of the C-ABI library (no GPU needed): the library loads, exports
+every symbol include/*.h declares, validates arguments before launching anything,
+and its host logic (closed-form nnz, LPT partitioner) matches the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2602_16986_b200 import uhstu as U
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = []
+    for h in ("uhstu.h", "uhstu_testing.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        names += re.findall(r"UH_API\s+[\w\s\*]+?\b(uh_\w+)\s*\(", txt)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert len(syms) >= 17
+    out = subprocess.run(["nm", "-D", "--defined-only", U.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\sT\s(uh_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    L = U.lib()
+    for s in syms:
+        assert hasattr(L, s)
+    assert L.uh_abi_version() == 1
+
+
+def test_mask_nnz_matches_oracle_enumeration():
+    for L in (0, 1, 2, 17, 40, 64, 129, 300):
+        for K1, K2 in ((16, 2), (0, 0), (1, 0), (5, 7), (U.WINDOW_FULL, 0), (128, 129), (300, 1)):
+            okK1 = O.FULL if K1 == U.WINDOW_FULL else K1
+            assert U.mask_nnz(U.mask(K1, K2), L) == O.mask_nnz(L, okK1, K2), (L, K1, K2)
+    assert U.mask_nnz(U.mask(1024, 128), 16384) == 18226624
+
+
+def test_partition_matches_oracle():
+    rng = np.random.default_rng(0)
+    for world in (1, 2, 3, 8):
+        lengths = [int(x) for x in rng.integers(1, 700, size=23)] + [700, 700, 1]
+        owner, cost = U.partition_lpt(lengths, world, U.mask(16, 2), 64, 2)
+        o_owner, o_load = O.partition_lpt(lengths, world, 64, 2, 16, 2)
+        assert list(owner) == o_owner
+        assert np.allclose(cost, o_load, rtol=1e-12)
+
+
+def test_partition_balances_cfg4_lengths():
+    from paper_2602_16986_b200 import synth
+    cfg = synth.config("cfg4", world=8)
+    owner, cost = U.partition_lpt(cfg.lengths, 8, U.mask(cfg.K1, cfg.K2), cfg.d, cfg.H)
+    assert sorted(set(owner.tolist())) == list(range(8))
+    assert cost.max() / cost.mean() < 1.01
+
+
+def _jag(offsets):
+    return U.JaggedBatch(offsets, device=None)
+
+
+def _status(fn):
+    with pytest.raises(U.UhError) as e:
+        fn()
+    return e.value.name
+
+
+def test_validation_errors_before_launch():
+    desc = U.Attn(2, 32, norm_n=64.0)
+    m = U.mask(16, 2)
+    ok = _jag([0, 17, 57, 121])
+    n = U.attn_workspace_bytes(ok, m, desc, U.F32, True)
+    assert n > 0
+    # bad offsets: decreasing -> DOMAIN; offsets[0] != 0 -> DIM
+    bad = _jag([0, 17, 10, 121])
+    assert _status(lambda: U.attn_workspace_bytes(bad, m, desc, U.F32, False)) == "UH_ERR_DOMAIN"
+    bad0 = _jag([3, 17, 57, 121])
+    assert _status(lambda: U.attn_workspace_bytes(bad0, m, desc, U.F32, False)) == "UH_ERR_DIM"
+    wrong_max = _jag([0, 17, 57, 121]); wrong_max.c.max_len = 7
+    assert _status(lambda: U.attn_workspace_bytes(wrong_max, m, desc, U.F32, False)) == "UH_ERR_DIM"
+    assert _status(lambda: U.attn_workspace_bytes(ok, U.Mask(-1, 0), desc, U.F32, False)) == "UH_ERR_DOMAIN"
+    assert _status(lambda: U.attn_workspace_bytes(ok, m, U.Attn(2, 48), U.F32, False)) == "UH_ERR_SHAPE"
+    assert _status(lambda: U.attn_workspace_bytes(ok, m, U.Attn(2, 32), U.BF16, False)) == "UH_ERR_UNSUPPORTED"
+    assert _status(lambda: U.attn_workspace_bytes(ok, m, U.Attn(2, 32, norm_n=0.0), U.F32, False)) == "UH_ERR_DOMAIN"
+    # empty batch is a valid no-op
+    assert U.attn_workspace_bytes(_jag([0]), m, desc, U.F32, False) >= 0
+
+
+def test_null_and_alignment_checks_fwd():
+    L = U.lib()
+    jag = _jag([0, 17])
+    jag.c.offsets = ctypes.c_void_p(0x1000)  # never dereferenced: checks fail first
+    d = U.Attn(1, 32, norm_n=1.0).c()
+    st = L.uh_attn_fwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(d), U.F32, None, None, None, 32,
+                       None, 32, None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_NULL"
+    st = L.uh_attn_fwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(d), U.F32, ctypes.c_void_p(0x1008),
+                       ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), 32, ctypes.c_void_p(0x1000), 32, None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_ALIGNMENT"
+    st = L.uh_attn_fwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(d), U.F32, ctypes.c_void_p(0x1000),
+                       ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), 30, ctypes.c_void_p(0x1000), 32, None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_DIM"
+    st = L.uh_attn_fwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(d), U.F32, ctypes.c_void_p(0x1000),
+                       ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), 32, ctypes.c_void_p(0x1000), 32, None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_WORKSPACE"
+
+
+def test_layer_bwd_requires_saved_set():
+    L = U.lib()
+    jag = _jag([0, 17])
+    jag.c.offsets = ctypes.c_void_p(0x1000)
+    p = U.LayerParams()
+    p.attn = U.Attn(2, 32, norm_n=1.0).c()
+    for f in ("ln1_w", "ln1_b", "w1", "ln2_w", "ln2_b", "w2"):
+        setattr(p, f, ctypes.c_void_p(0x1000))
+    p.eps = 1e-6
+    g = U.LayerGrads()
+    st = L.uh_layer_bwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(p), U.F32, ctypes.c_void_p(0x1000), None,
+                        ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), ctypes.byref(g), 0, None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_CACHE_MISMATCH"
