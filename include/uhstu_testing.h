@@ -15,6 +15,8 @@ extern "C" {
 UH_API uh_status uh_test_gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb,
                               int b_mn, int epi, void* out0, int64_t ld0, void* out1, int64_t ld1, const float* bias,
                               const void* resid, int64_t ldr, uh_dtype dtype, void* stream);
+/* Number of kernels the library has launched in this process (all entry points). */
+UH_API long long uh_test_launch_count(void);
 #ifdef __cplusplus
 }
 #endif

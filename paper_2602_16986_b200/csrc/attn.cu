@@ -138,6 +138,7 @@ static uh_status schedule(const AttnCall& c, uh_dtype dt, int mode, WorkItem* it
     const int BNt = dt == UH_BF16 ? 128 : 32;
     build_schedule_k<<<1, kSchedThreads, 0, c.st>>>(c.jag->offsets, c.jag->num_seqs, c.desc->num_heads, BMt, BNt,
                                                     c.mask.window, c.mask.n_global, mode, items, counter);
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }

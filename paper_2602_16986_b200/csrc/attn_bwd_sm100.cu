@@ -1,9 +1,598 @@
-// attn_bwd_sm100.cu — placeholder until the tcgen05 backward lands.
+// attn_bwd_sm100.cu — jagged semi-local HSTU attention backward on tcgen05.
+//
+// Listing 1's "dq, dk, dv = attention_backward(dattn, q, k, v)" for the
+// forward of attn_fwd_sm100.cu (Eq. 3; SLA P:140-146; R5-R7):
+//     p = silu(s)/N, ds = dP * silu'(s)/N, dP = dA V^T, s = alpha Q K^T + rab
+//     dV = P^T dA,  dK = alpha dS^T Q,  dQ = alpha dS K,  d rab = scatter-sum of ds.
+// Two kernels, no fp32 atomics on the [T,d] gradients:
+//   dq kernel  (query-major): per 128-query tile, over its visible 64-key tiles:
+//              S, dP (TMEM, double-buffered) -> dS (bf16 smem) -> dQ += dS K (TMEM).
+//              Also reduces d pos_bias / d time_bias (run-length + diagonal sums).
+//   dkv kernel (key-major):   per 128-key tile, over the 64-query tiles that see it:
+//              S^T, dP^T (TMEM, double-buffered) -> P^T, dS^T (bf16 smem)
+//              -> dV += P^T dA, dK += dS^T Q (TMEM).
+// Gradients are multiplied by optional gates (silu'(h), the layer's fused
+// "silu_backward") and written straight into their slices of dH (no
+// concat).
+#include <climits>
+
 #include "attn_common.cuh"
 #include "internal.h"
+
 namespace uh {
-uh_status attn_bwd_sm100_launch(const AttnArgs& a, const AttnArgs& akv, cudaStream_t st, int64_t T) {
-    (void)a; (void)akv; (void)st; (void)T;
-    return fail(UH_ERR_UNSUPPORTED, "bf16 attention backward not built yet");
+namespace {
+
+constexpr int DH = 128;
+constexpr int NUM_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue
+
+__device__ __forceinline__ void store_bf16_row32(uint8_t* tile, int r, int col0, const float* v) {
+    // row r of a [rows x 64] bf16 K-major SW128 tile; 32 columns starting at col0 (0 or 32)
+    uint8_t* row = tile + r * 128;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int ch = (col0 >> 3) + c;
+        uint4 u = make_uint4(pack_bf16(v[c * 8 + 0], v[c * 8 + 1]), pack_bf16(v[c * 8 + 2], v[c * 8 + 3]),
+                             pack_bf16(v[c * 8 + 4], v[c * 8 + 5]), pack_bf16(v[c * 8 + 6], v[c * 8 + 7]));
+        *reinterpret_cast<uint4*>(row + ((ch ^ (r & 7)) << 4)) = u;
+    }
 }
+
+__device__ __forceinline__ float load_bf16_sw(const uint8_t* tile, int r, int c) {
+    const uint8_t* p = tile + r * 128 + ((((c >> 3) ^ (r & 7))) << 4) + (c & 7) * 2;
+    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p));
+}
+
+__device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t row, int col, const float* v,
+                                                const void* gate, int64_t ldg, float scale) {
+    float w[64];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) w[c] = v[c] * scale;
+    if (gate) {
+        const uint4* g = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(gate) + row * ldg + col);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            uint4 gv = __ldg(g + ch);
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float2 f = __bfloat1622float2(g2[e]);
+                w[ch * 8 + 2 * e] *= f.x;
+                w[ch * 8 + 2 * e + 1] *= f.y;
+            }
+        }
+    }
+    uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + row * ld + col);
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch)
+        o[ch] = make_uint4(pack_bf16(w[ch * 8 + 0], w[ch * 8 + 1]), pack_bf16(w[ch * 8 + 2], w[ch * 8 + 3]),
+                           pack_bf16(w[ch * 8 + 4], w[ch * 8 + 5]), pack_bf16(w[ch * 8 + 6], w[ch * 8 + 7]));
+}
+
+// bias of 32 consecutive columns: fills b[32]; qpos/kpos of column c = q0c + c*dq, k0c + c*dk
+struct RabRow {
+    const AttnArgs* a;
+    int o;
+};
+
+// ============================================================================ dq kernel
+namespace dq {
+constexpr int BM = 128, BN = 64;
+constexpr int QT = 128 * 128 * 2;       // Q / dA tile bytes (2 x 16K blocks)
+constexpr int KT = 64 * 128 * 2;        // K / V tile bytes (2 x 8K blocks)
+constexpr int ST = 128 * 64 * 2;        // dS tile (1 block)
+constexpr int KV_STAGES = 3;
+constexpr int SMEM = 2 * QT + KV_STAGES * 2 * KT + 2 * ST + 1024 + 512;
+
+struct __align__(8) Bars {
+    uint64_t qa_full, qa_empty;
+    uint64_t kv_full[KV_STAGES], kv_empty[KV_STAGES];
+    uint64_t s_full[2], s_empty[2];
+    uint64_t ds_full[2], ds_empty[2];
+    uint64_t dq_full, dq_empty;
+    uint32_t tmem;
+    float dts[64];
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sdA = smem + QT;
+    uint8_t* sK = smem + 2 * QT;                      // [KV_STAGES]
+    uint8_t* sV = sK + KV_STAGES * KT;                // [KV_STAGES]
+    uint8_t* sdS = sV + KV_STAGES * KT;               // [2]
+    Bars* bars = reinterpret_cast<Bars*>(sdS + 2 * ST);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->qa_full, 1); mbar_init(&bars->qa_empty, 1);
+        for (int i = 0; i < KV_STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->s_full[i], 1); mbar_init(&bars->s_empty[i], 8);
+            mbar_init(&bars->ds_full[i], 8); mbar_init(&bars->ds_empty[i], 1);
+        }
+        mbar_init(&bars->dq_full, 1); mbar_init(&bars->dq_empty, 8);
+        fence_barrier_init();
+    }
+    if (threadIdx.x < 64) bars->dts[threadIdx.x] = 0.f;
+    if (warp == 2) tmem_alloc<512>(&bars->tmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int kc = 0, qi = 0;
+            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+                const WorkItem it = a.items[w];
+                const int q0 = it.tile * BM, h = it.head & 0xFFFF;
+                const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
+                const int n = key_tiles_count(kt);
+                mbar_wait(&bars->qa_empty, (qi & 1) ^ 1);
+                mbar_arrive_expect_tx(&bars->qa_full, 2 * QT);
+                tma_load_2d(sQ, &tmQ, &bars->qa_full, h * DH, it.seq_start + q0);
+                tma_load_2d(sQ + QT / 2, &tmQ, &bars->qa_full, h * DH + 64, it.seq_start + q0);
+                tma_load_2d(sdA, &tmdA, &bars->qa_full, h * DH, it.seq_start + q0);
+                tma_load_2d(sdA + QT / 2, &tmdA, &bars->qa_full, h * DH + 64, it.seq_start + q0);
+                for (int j = 0; j < n; ++j) {
+                    const int row = it.seq_start + key_tile_at(kt, j) * BN;
+                    const int s = kc % KV_STAGES;
+                    mbar_wait(&bars->kv_empty[s], ((kc / KV_STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
+                    tma_load_2d(sK + s * KT, &tmK, &bars->kv_full[s], h * DH, row);
+                    tma_load_2d(sK + s * KT + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
+                    tma_load_2d(sV + s * KT, &tmV, &bars->kv_full[s], h * DH, row);
+                    tma_load_2d(sV + s * KT + KT / 2, &tmV, &bars->kv_full[s], h * DH + 64, row);
+                    ++kc;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // Q x K^T, dA x V^T
+        constexpr uint32_t idesc_q = make_idesc_bf16(BM, DH, false, true);    // dS (K-major) x K (MN-major)
+        int kc = 0, sc = 0, dc = 0, qi = 0;
+        const uint32_t q_addr = smem_u32(sQ), da_addr = smem_u32(sdA);
+        auto issue_dq = [&](int jj, int kstage) {
+            const int db = dc & 1;
+            mbar_wait(&bars->ds_full[db], (dc >> 1) & 1);
+            if (jj == 0) mbar_wait(&bars->dq_empty, (qi & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t ds_addr = smem_u32(sdS + db * ST);
+                const uint32_t k_addr = smem_u32(sK + kstage * KT);
+#pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk)
+                    umma_ss(tmem + 256, make_sw128_desc(ds_addr + kk * 32, 16, 1024),
+                            make_sw128_desc(k_addr + kk * 2048, KT / 2, 1024), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&bars->ds_empty[db]);
+                umma_commit(&bars->kv_empty[kstage]);
+            }
+            __syncwarp();
+            ++dc;
+        };
+        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+            const WorkItem it = a.items[w];
+            const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
+            const int n = key_tiles_count(kt);
+            mbar_wait(&bars->qa_full, qi & 1);
+            int prev_stage = 0;
+            for (int j = 0; j < n; ++j) {
+                const int s = kc % KV_STAGES, sb = sc & 1;
+                mbar_wait(&bars->kv_full[s], (kc / KV_STAGES) & 1);
+                mbar_wait(&bars->s_empty[sb], ((sc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t k_addr = smem_u32(sK + s * KT), v_addr = smem_u32(sV + s * KT);
+#pragma unroll
+                    for (int kk = 0; kk < DH / 16; ++kk) {
+                        const uint32_t oa = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
+                        const uint32_t ob = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
+                        umma_ss(tmem + sb * BN, make_sw128_desc(q_addr + oa, 16, 1024),
+                                make_sw128_desc(k_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                        umma_ss(tmem + 128 + sb * BN, make_sw128_desc(da_addr + oa, 16, 1024),
+                                make_sw128_desc(v_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&bars->s_full[sb]);
+                    if (j == n - 1) umma_commit(&bars->qa_empty);
+                }
+                __syncwarp();
+                ++sc;
+                if (j >= 1) issue_dq(j - 1, prev_stage);
+                prev_stage = s;
+                ++kc;
+            }
+            issue_dq(n - 1, prev_stage);
+            if (elect_one()) umma_commit(&bars->dq_full);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const int wg = (warp - 4) >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        const int et = threadIdx.x - 128;  // 0..255 among epilogue threads
+        int sc = 0, dc = 0, qi = 0;
+        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+            const WorkItem it = a.items[w];
+            const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
+            const int q0 = it.tile * BM;
+            const KeyTiles kt = key_tiles(q0, BM, L, a.K1, a.K2, BN);
+            const int n = key_tiles_count(kt);
+            const int qp = q0 + r;
+            const bool qok = qp < L;
+            const int64_t tq = (a.ts && qok) ? __ldg(a.t + o + qp) : 0;
+            float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals)
+            int cur_b = -1;            // d time_bias run-length state
+            float cur_acc = 0.f;
+            for (int j = 0; j < n; ++j) {
+                const int k0 = key_tile_at(kt, j) * BN;
+                const int kbase = k0 + wg * 32;
+                const int sb = sc & 1;
+                mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
+                tc_fence_after();
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + sb * BN + wg * 32, sv);
+                tmem_ld32(tmem + lane_base + 128 + sb * BN + wg * 32, dp);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
+                ++sc;
+                // ---- bias (per 32-column chunk: constant fast path when possible)
+                const bool full_tile = qok && (kbase + 31 <= qp) && (qp - kbase <= a.K1 || kbase + 31 < a.K2);
+                float pos_c = 0.f, ts_c = 0.f;
+                bool pos_const = true, ts_const = true;
+                int b_hi = 0;
+                if (a.pos) {
+                    pos_const = qp - (kbase + 31) >= a.P - 1;
+                    if (pos_const) pos_c = __ldg(a.pos + a.P - 1);
+                }
+                if (a.ts) {
+                    const int kl = imin(kbase + 31, L - 1), kf = imin(kbase, L - 1);
+                    b_hi = time_bucket(tq - __ldg(a.t + o + kf), a.NB);
+                    const int b_lo = time_bucket(tq - __ldg(a.t + o + kl), a.NB);
+                    ts_const = full_tile && b_hi == b_lo;
+                    if (ts_const) ts_c = __ldg(a.ts + b_hi);
+                }
+                float ds[32];
+                float tile_sum = 0.f;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int kp = kbase + c;
+                    const bool ok = full_tile || (qok && kp < L && mask_ok(qp, kp, a.K1, a.K2));
+                    float x = a.alpha * sv[c] + pos_c + ts_c;
+                    if (ok && (!pos_const || !ts_const)) {
+                        if (!pos_const) { int dd = qp - kp; x += __ldg(a.pos + (dd < a.P - 1 ? dd : a.P - 1)); }
+                        if (!ts_const) x += __ldg(a.ts + time_bucket(tq - __ldg(a.t + o + kp), a.NB));
+                    }
+                    const float sg = __frcp_rn(1.0f + __expf(-x));
+                    const float v = dp[c] * sg * (1.0f + x * (1.0f - sg)) * a.inv_n;
+                    ds[c] = ok ? v : 0.f;
+                    tile_sum += ds[c];
+                }
+                // ---- d time_bias: run-length over buckets (non-increasing along the row)
+                if (a.dts) {
+                    if (ts_const) {
+                        if (b_hi != cur_b) { if (cur_b >= 0) atomicAdd(&bars->dts[cur_b], cur_acc); cur_b = b_hi; cur_acc = 0.f; }
+                        cur_acc += tile_sum;
+                    } else {
+#pragma unroll 1
+                        for (int c = 0; c < 32; ++c) {
+                            if (ds[c] == 0.f) continue;
+                            const int b = time_bucket(tq - __ldg(a.t + o + kbase + c), a.NB);
+                            if (b != cur_b) { if (cur_b >= 0) atomicAdd(&bars->dts[cur_b], cur_acc); cur_b = b; cur_acc = 0.f; }
+                            cur_acc += ds[c];
+                        }
+                    }
+                }
+                far_acc += tile_sum;
+                // ---- dS (bf16) -> smem for dQ += dS K
+                const int db = dc & 1;
+                mbar_wait(&bars->ds_empty[db], ((dc >> 1) & 1) ^ 1);
+                uint8_t* tile = sdS + db * ST;
+                store_bf16_row32(tile, r, wg * 32, ds);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->ds_full[db]);
+                ++dc;
+                // ---- d pos_bias near diagonals (delta <= P-2) from the bf16 dS tile
+                if (a.dpos) {
+                    const int D0 = q0 - k0;
+                    const int lo = imax(0, D0 - (BN - 1)), hi = imin(a.P - 2, D0 + BM - 1);
+                    if (lo <= hi) {
+                        named_bar_sync(1, 256);
+                        const int nd = hi - lo + 1;
+                        for (int idx = et; idx < nd * 4; idx += 256) {
+                            const int delta = lo + (idx >> 2), part = idx & 3;
+                            float sum = 0.f;
+                            // rows i with j = i + D0 - delta in [0, BN)
+                            const int i0 = imax(0, delta - D0), i1 = imin(BM, delta - D0 + BN);
+                            for (int i = i0 + part; i < i1; i += 4) sum += load_bf16_sw(tile, i, i + D0 - delta);
+                            if (sum != 0.f) { atomicAdd(a.dpos + delta, sum); far_acc -= sum; }
+                        }
+                        named_bar_sync(1, 256);
+                    }
+                }
+            }
+            // ---- flush rab partials of this item
+            if (a.dts && cur_b >= 0) atomicAdd(&bars->dts[cur_b], cur_acc);
+            if (a.dpos) {
+                float f = far_acc;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
+                if (lane == 0 && f != 0.f) atomicAdd(a.dpos + a.P - 1, f);
+            }
+            // ---- dQ epilogue
+            mbar_wait(&bars->dq_full, qi & 1);
+            tc_fence_after();
+            float v[64];
+            tmem_ld32(tmem + lane_base + 256 + wg * 64, v);
+            tmem_ld32(tmem + lane_base + 256 + wg * 64 + 32, v + 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->dq_empty);
+            if (qok) store_out_row64(a.dq, a.ld_grad, o + qp, h * DH + wg * 64, v, a.gq, a.ld_gate, a.alpha);
+        }
+    }
+    __syncthreads();
+    if (a.dts && threadIdx.x < a.NB && bars->dts[threadIdx.x] != 0.f) atomicAdd(a.dts + threadIdx.x, bars->dts[threadIdx.x]);
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+}  // namespace dq
+
+// ============================================================================ dkv kernel
+namespace dkv {
+constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per tile
+constexpr int KT = 128 * 128 * 2;         // K / V tile bytes
+constexpr int QT = 64 * 128 * 2;          // Q / dA tile bytes
+constexpr int PT = 128 * 64 * 2;          // P^T / dS^T tile bytes
+constexpr int QA_STAGES = 3;
+constexpr int SMEM = 2 * KT + QA_STAGES * 2 * QT + 2 * PT + 1024 + 512;
+
+struct __align__(8) Bars {
+    uint64_t kv_full, kv_empty;
+    uint64_t qa_full[QA_STAGES], qa_empty[QA_STAGES];
+    uint64_t s_full[2], s_empty[2];
+    uint64_t p_full, p_empty;
+    uint64_t acc_full, acc_empty;
+    uint32_t tmem;
+};
+
+__device__ __forceinline__ int n_qtiles(int k0, int L, int K1, int K2) {
+    const int qe = query_end(k0, BM, L, K1, K2);
+    const int first = k0 / BN;
+    return (qe + BN - 1) / BN - first;
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sV = smem + KT;
+    uint8_t* sQ = smem + 2 * KT;                 // [QA_STAGES]
+    uint8_t* sdA = sQ + QA_STAGES * QT;          // [QA_STAGES]
+    uint8_t* sP = sdA + QA_STAGES * QT;
+    uint8_t* sdS = sP + PT;
+    Bars* bars = reinterpret_cast<Bars*>(sdS + PT);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->kv_full, 1); mbar_init(&bars->kv_empty, 1);
+        for (int i = 0; i < QA_STAGES; ++i) { mbar_init(&bars->qa_full[i], 1); mbar_init(&bars->qa_empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->s_empty[i], 8); }
+        mbar_init(&bars->p_full, 8); mbar_init(&bars->p_empty, 1);
+        mbar_init(&bars->acc_full, 1); mbar_init(&bars->acc_empty, 8);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(&bars->tmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int qc = 0, ki = 0;
+            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+                const WorkItem it = a.items[w];
+                const int k0 = it.tile * BM, h = it.head & 0xFFFF;
+                const int n = n_qtiles(k0, it.seq_len, a.K1, a.K2);
+                mbar_wait(&bars->kv_empty, (ki & 1) ^ 1);
+                mbar_arrive_expect_tx(&bars->kv_full, 2 * KT);
+                tma_load_2d(sK, &tmK, &bars->kv_full, h * DH, it.seq_start + k0);
+                tma_load_2d(sK + KT / 2, &tmK, &bars->kv_full, h * DH + 64, it.seq_start + k0);
+                tma_load_2d(sV, &tmV, &bars->kv_full, h * DH, it.seq_start + k0);
+                tma_load_2d(sV + KT / 2, &tmV, &bars->kv_full, h * DH + 64, it.seq_start + k0);
+                for (int i = 0; i < n; ++i) {
+                    const int row = it.seq_start + (k0 / BN + i) * BN;
+                    const int s = qc % QA_STAGES;
+                    mbar_wait(&bars->qa_empty[s], ((qc / QA_STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bars->qa_full[s], 2 * QT);
+                    tma_load_2d(sQ + s * QT, &tmQ, &bars->qa_full[s], h * DH, row);
+                    tma_load_2d(sQ + s * QT + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
+                    tma_load_2d(sdA + s * QT, &tmdA, &bars->qa_full[s], h * DH, row);
+                    tma_load_2d(sdA + s * QT + QT / 2, &tmdA, &bars->qa_full[s], h * DH + 64, row);
+                    ++qc;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // K x Q^T, V x dA^T
+        constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // P^T (K-major) x dA (MN-major)
+        int qc = 0, sc = 0, pc = 0, ki = 0;
+        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+        auto issue_acc = [&](int ii, int st) {
+            mbar_wait(&bars->p_full, pc & 1);
+            if (ii == 0) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t p_addr = smem_u32(sP), ds_addr = smem_u32(sdS);
+                const uint32_t da_addr = smem_u32(sdA + st * QT), q_addr = smem_u32(sQ + st * QT);
+#pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk) {
+                    umma_ss(tmem + 256, make_sw128_desc(p_addr + kk * 32, 16, 1024),
+                            make_sw128_desc(da_addr + kk * 2048, QT / 2, 1024), idesc_a, (ii > 0 || kk > 0) ? 1u : 0u);
+                    umma_ss(tmem + 384, make_sw128_desc(ds_addr + kk * 32, 16, 1024),
+                            make_sw128_desc(q_addr + kk * 2048, QT / 2, 1024), idesc_a, (ii > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&bars->p_empty);
+                umma_commit(&bars->qa_empty[st]);
+            }
+            __syncwarp();
+            ++pc;
+        };
+        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+            const WorkItem it = a.items[w];
+            const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+            mbar_wait(&bars->kv_full, ki & 1);
+            int prev = 0;
+            for (int i = 0; i < n; ++i) {
+                const int s = qc % QA_STAGES, sb = sc & 1;
+                mbar_wait(&bars->qa_full[s], (qc / QA_STAGES) & 1);
+                mbar_wait(&bars->s_empty[sb], ((sc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t q_addr = smem_u32(sQ + s * QT), da_addr = smem_u32(sdA + s * QT);
+#pragma unroll
+                    for (int kk = 0; kk < DH / 16; ++kk) {
+                        const uint32_t oa = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
+                        const uint32_t ob = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
+                        umma_ss(tmem + sb * BN, make_sw128_desc(k_addr + oa, 16, 1024),
+                                make_sw128_desc(q_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                        umma_ss(tmem + 128 + sb * BN, make_sw128_desc(v_addr + oa, 16, 1024),
+                                make_sw128_desc(da_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&bars->s_full[sb]);
+                    if (i == n - 1) umma_commit(&bars->kv_empty);
+                }
+                __syncwarp();
+                ++sc;
+                if (i >= 1) issue_acc(i - 1, prev);
+                prev = s;
+                ++qc;
+            }
+            issue_acc(n - 1, prev);
+            if (elect_one()) umma_commit(&bars->acc_full);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        const int wg = (warp - 4) >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        int sc = 0, pc = 0, ki = 0;
+        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+            const WorkItem it = a.items[w];
+            const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
+            const int k0 = it.tile * BM;
+            const int n = n_qtiles(k0, L, a.K1, a.K2);
+            const int kp = k0 + r;
+            const bool kok = kp < L;
+            const int64_t tk = (a.ts && kok) ? __ldg(a.t + o + kp) : 0;
+            for (int i = 0; i < n; ++i) {
+                const int qbase = (k0 / BN + i) * BN + wg * 32;
+                const int sb = sc & 1;
+                mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
+                tc_fence_after();
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + sb * BN + wg * 32, sv);
+                tmem_ld32(tmem + lane_base + 128 + sb * BN + wg * 32, dp);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
+                ++sc;
+                // all 32 (q, kp) allowed?  q in [qbase, qbase+31]
+                const bool full_tile = kok && (qbase >= kp) && (qbase + 31 < L) &&
+                                       (qbase + 31 - kp <= a.K1 || kp < a.K2);
+                float pos_c = 0.f, ts_c = 0.f;
+                bool pos_const = true, ts_const = true;
+                if (a.pos) {
+                    pos_const = qbase - kp >= a.P - 1;
+                    if (pos_const) pos_c = __ldg(a.pos + a.P - 1);
+                }
+                if (a.ts) {
+                    const int ql = imin(qbase + 31, L - 1), qf = imin(qbase, L - 1);
+                    const int b_lo = time_bucket(__ldg(a.t + o + qf) - tk, a.NB);
+                    const int b_hi = time_bucket(__ldg(a.t + o + ql) - tk, a.NB);
+                    ts_const = full_tile && b_hi == b_lo;
+                    if (ts_const) ts_c = __ldg(a.ts + b_lo);
+                }
+                float p[32], ds[32];
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const int qp = qbase + c;
+                    const bool ok = full_tile || (kok && qp < L && mask_ok(qp, kp, a.K1, a.K2));
+                    float x = a.alpha * sv[c] + pos_c + ts_c;
+                    if (ok && (!pos_const || !ts_const)) {
+                        if (!pos_const) { int dd = qp - kp; x += __ldg(a.pos + (dd < a.P - 1 ? dd : a.P - 1)); }
+                        if (!ts_const) x += __ldg(a.ts + time_bucket(__ldg(a.t + o + qp) - tk, a.NB));
+                    }
+                    const float sg = __frcp_rn(1.0f + __expf(-x));
+                    p[c] = ok ? x * sg * a.inv_n : 0.f;
+                    ds[c] = ok ? a.alpha * dp[c] * sg * (1.0f + x * (1.0f - sg)) * a.inv_n : 0.f;
+                }
+                mbar_wait(&bars->p_empty, (pc & 1) ^ 1);
+                store_bf16_row32(sP, r, wg * 32, p);
+                store_bf16_row32(sdS, r, wg * 32, ds);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->p_full);
+                ++pc;
+            }
+            mbar_wait(&bars->acc_full, ki & 1);
+            tc_fence_after();
+            float dv[64], dk[64];
+            tmem_ld32(tmem + lane_base + 256 + wg * 64, dv);
+            tmem_ld32(tmem + lane_base + 256 + wg * 64 + 32, dv + 32);
+            tmem_ld32(tmem + lane_base + 384 + wg * 64, dk);
+            tmem_ld32(tmem + lane_base + 384 + wg * 64 + 32, dk + 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->acc_empty);
+            if (kok) {
+                store_out_row64(a.dv, a.ld_grad, o + kp, h * DH + wg * 64, dv, a.gv, a.ld_gate, 1.0f);
+                store_out_row64(a.dk, a.ld_grad, o + kp, h * DH + wg * 64, dk, a.gk, a.ld_gate, 1.0f);
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+}  // namespace dkv
+
+}  // namespace
+
+uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStream_t st, int64_t T) {
+    if (aq.dh != DH) return fail(UH_ERR_UNSUPPORTED, "bf16 attention requires head_dim == 128");
+    if (aq.n_items == 0) return UH_OK;
+    const uint64_t width = (uint64_t)aq.H * DH;
+    CUtensorMap q128, dA128, k64, v64;
+    UH_TRY(make_tmap_bf16(&q128, aq.q, width, T, aq.ld_qkv, 64, 128));
+    UH_TRY(make_tmap_bf16(&dA128, aq.dout, width, T, aq.ld_dout, 64, 128));
+    UH_TRY(make_tmap_bf16(&k64, aq.k, width, T, aq.ld_qkv, 64, 64));
+    UH_TRY(make_tmap_bf16(&v64, aq.v, width, T, aq.ld_qkv, 64, 64));
+    UH_CUDA(cudaFuncSetAttribute(dq::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dq::SMEM));
+    const int sms = num_sms();
+    dq::kernel<<<aq.n_items < sms ? aq.n_items : sms, NUM_THREADS, dq::SMEM, st>>>(q128, k64, v64, dA128, aq);
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+
+    CUtensorMap q64, dA64, k128, v128;
+    UH_TRY(make_tmap_bf16(&q64, akv.q, width, T, akv.ld_qkv, 64, 64));
+    UH_TRY(make_tmap_bf16(&dA64, akv.dout, width, T, akv.ld_dout, 64, 64));
+    UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));
+    UH_TRY(make_tmap_bf16(&v128, akv.v, width, T, akv.ld_qkv, 64, 128));
+    UH_CUDA(cudaFuncSetAttribute(dkv::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv::SMEM));
+    dkv::kernel<<<akv.n_items < sms ? akv.n_items : sms, NUM_THREADS, dkv::SMEM, st>>>(q64, k128, v128, dA64, akv);
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
 }  // namespace uh

@@ -262,6 +262,7 @@ uh_status attn_fwd_sm100_launch(const AttnArgs& a, cudaStream_t st, int64_t T) {
     UH_CUDA(cudaFuncSetAttribute(attn_fwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     const int grid = a.n_items < num_sms() ? a.n_items : num_sms();
     attn_fwd_sm100<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(tq, tk, tv, a);
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }

@@ -244,6 +244,7 @@ uh_status attn_fwd_simt_launch(const AttnArgs& a, cudaStream_t st) {
         case 128: attn_fwd_simt<128><<<a.n_items, 256, 0, st>>>(a); break;
         default: return fail(UH_ERR_SHAPE, "fp32 attention: head_dim must be 32, 64 or 128");
     }
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -256,6 +257,8 @@ uh_status attn_bwd_simt_launch(const AttnArgs& a, cudaStream_t st) {
         case 128: attn_dq_simt<128><<<a.n_items, 256, 0, st>>>(a); attn_dkv_simt<128><<<a.n_items, 256, 0, st>>>(a); break;
         default: return fail(UH_ERR_SHAPE, "fp32 attention: head_dim must be 32, 64 or 128");
     }
+    note_launch();
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }

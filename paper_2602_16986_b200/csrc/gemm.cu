@@ -85,14 +85,17 @@ static uh_status gemm_f32(const GemmDesc& g, cudaStream_t st) {
         case EPI_BF16:
             gemm_f32_simt<EPI_BF16><<<grid, 256, 0, st>>>(g.M, g.N, g.K, A, sam, sak, B, sbk, sbn, (float*)g.out0, g.ld0,
                                                          (float*)g.out1, g.ld1, g.bias, (const float*)g.resid, g.ldr, kchunk);
+            note_launch();
             break;
         case EPI_SILU:
             gemm_f32_simt<EPI_SILU><<<grid, 256, 0, st>>>(g.M, g.N, g.K, A, sam, sak, B, sbk, sbn, (float*)g.out0, g.ld0,
                                                          (float*)g.out1, g.ld1, g.bias, (const float*)g.resid, g.ldr, kchunk);
+            note_launch();
             break;
         default:
             gemm_f32_simt<EPI_F32><<<grid, 256, 0, st>>>(g.M, g.N, g.K, A, sam, sak, B, sbk, sbn, (float*)g.out0, g.ld0,
                                                         (float*)g.out1, g.ld1, g.bias, (const float*)g.resid, g.ldr, kchunk);
+            note_launch();
     }
     UH_CUDA(cudaGetLastError());
     return UH_OK;
@@ -130,6 +133,7 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
         attr_set = true;
     }
     kern<<<std::min(total, sms), 256, C::SMEM, st>>>(ta, tb, a);
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }

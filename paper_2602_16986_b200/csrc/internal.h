@@ -30,6 +30,8 @@ uh_status cuda_fail(cudaError_t e, const char* where);
 uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                          uint32_t box_inner, uint32_t box_outer);
 int num_sms();
+// every kernel launch of the library is counted (bench.py reports gpu_launches from it)
+void note_launch();
 
 // ------------------------------------------------------------------ GEMM
 // C[M,N] = A[M,K] * B[K,N].  a_mn: A stored [K][M] (else [M][K]); b_mn: B stored

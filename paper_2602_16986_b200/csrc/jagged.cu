@@ -54,6 +54,7 @@ uh_status run_segments(const std::vector<Seg>& segs, const void* x, int64_t ldx_
         dim3 grid((unsigned)std::min(64, (maxlen + 7) / 8), (unsigned)b.n);
         if (zero) zero_rows_k<<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
         else copy_rows_k<<<grid, 256, 0, st>>>(b, (const uint8_t*)x, ldx_bytes, (uint8_t*)y, ldy_bytes, row_bytes);
+        note_launch();
         UH_CUDA(cudaGetLastError());
     }
     return UH_OK;

@@ -389,6 +389,7 @@ uh_status ln_fwd(uh_dtype dt, int64_t T_, int d, const void* x, int64_t ldx, con
     if (T_ == 0) return UH_OK;
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         ln_fwd_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)x, ldx, w, b, eps, (T*)y, ldy, mean, rstd)));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -398,6 +399,7 @@ uh_status ln_apply(uh_dtype dt, int64_t T_, int d, const void* x, int64_t ldx, c
     if (T_ == 0) return UH_OK;
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         ln_apply_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)x, ldx, w, b, mean, rstd, (T*)y, ldy)));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -409,6 +411,7 @@ uh_status gated_norm_fwd(uh_dtype dt, int64_t T_, int d, const void* A, int64_t 
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         gated_fwd_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)A, lda, (const T*)U, ldu, w, b, eps,
                                                            (T*)Y, ldy, mean, rstd)));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -422,6 +425,7 @@ uh_status gated_norm_bwd(uh_dtype dt, int64_t T_, int d, const void* dY, int64_t
         gated_bwd_k<T, CPL><<<grid_persistent(T_), 256, 2 * d * sizeof(float), st>>>(
             T_, d, (const T*)dY, lddy, (const T*)A, lda, (const T*)U, ldu, (const T*)GU, ldg, w, b, mean, rstd,
             (T*)dA, ldda, (T*)dHU, ldh, (T*)Y, ldy, dw, db)));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -433,6 +437,7 @@ uh_status ln_bwd(uh_dtype dt, int64_t T_, int d, const void* dxh, int64_t ldg, c
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         ln_bwd_k<T, CPL><<<grid_persistent(T_), 256, 2 * d * sizeof(float), st>>>(
             T_, d, (const T*)dxh, ldg, (const T*)x, ldx, w, mean, rstd, (const T*)dres, ldr, (T*)dx, lddx, dw, db)));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -446,6 +451,7 @@ uh_status colsum(uh_dtype dt, int64_t T_, int n, const void* M, int64_t ldm, flo
     ry = (T_ + rpb - 1) / rpb;
     dim3 grid((unsigned)cols_blocks, (unsigned)ry);
     UH_DT_DISPATCH(dt, colsum_k<T><<<grid, 256, 0, st>>>(T_, n, (const T*)M, ldm, rpb, out));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
@@ -454,6 +460,7 @@ uh_status scale_store(uh_dtype dt, int64_t T_, int n, const float* acc, int64_t 
                       void* dst, int64_t ldd, cudaStream_t st) {
     if (T_ == 0 || n == 0) return UH_OK;
     UH_DT_DISPATCH(dt, scale_store_k<T><<<4 * num_sms(), 256, 0, st>>>(T_, n, acc, lda, (const T*)G, ldg, (T*)dst, ldd));
+    note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }

@@ -2,10 +2,12 @@
 // driver entry point for TMA descriptors, device properties.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 
 #include "internal.h"
+#include "../../include/uhstu_testing.h"
 
 namespace uh {
 
@@ -54,6 +56,10 @@ uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint
     return UH_OK;
 }
 
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
+
 int num_sms() {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -68,3 +74,5 @@ int num_sms() {
 }  // namespace uh
 
 extern "C" const char* uh_last_error(void) { return uh::g_last_error.c_str(); }
+
+extern "C" long long uh_test_launch_count(void) { return uh::launch_count(); }

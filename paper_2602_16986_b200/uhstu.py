@@ -99,10 +99,16 @@ def lib():
         L.uh_test_gemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, i64, ctypes.c_int, vp, i64,
                                    ctypes.c_int, ctypes.c_int, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp]
         L.uh_test_gemm.restype = ctypes.c_int
+        L.uh_test_launch_count.restype = ctypes.c_longlong
         if L.uh_abi_version() != 1:
             raise RuntimeError("libuhstu ABI version mismatch")
         _lib = L
     return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libuhstu so far in this process."""
+    return int(lib().uh_test_launch_count())
 
 
 def exported_symbols() -> list:
