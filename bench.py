@@ -1,0 +1,363 @@
+"""bench.py — throughput of the ULTRA-HSTU hot path on B200 (BASELINE.json metric:
+"HSTU attn effective TFLOP/s & tokens/s at L=16k vs bf16 peak, 1/2/4/8 B200").
+
+A step = one pass of the whole hot path over one batch of synthetic
+input: the jagged schedule, LN, f1+SiLU, SLA attention, gated norm, f2+residual
+(forward), then the rematerialising backward (LN apply, f1 remat, dY/dW2, gated-norm
+backward, attention backward, dW1/dx^, LN backward) and — for N > 1 — the NCCL
+all-reduce of the layer's fp32 weight-gradient bucket.  Each rank runs the cfg3
+shape (16 x 16384 tokens, 4 heads x 128, window 1024 + 128 global, rab on), so
+per-GPU work is fixed as N grows ("scaling": "weak"); the global batch is sharded by
+the LPT token-balanced partitioner (uh_partition_lpt).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg3|cfg2|cfg4]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HSTU attn effective TFLOP/s & tokens/s at L=16k vs bf16 peak, 1/2/4/8 B200"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"bf16_tflops": d["bf16_tflops"], "bf16_tflops_sustained": d.get("bf16_tflops_sustained"),
+                "hbm_gbs": d["hbm_gbs"], "source": "measured"}
+    except Exception:
+        return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+def setup_workload(cfg_name: str, world: int, rank: int, device):
+    import torch
+
+    from paper_2602_16986_b200 import synth
+    from paper_2602_16986_b200 import uhstu as U
+
+    gcfg = synth.config(cfg_name, world=world)
+    m = U.mask(gcfg.K1, gcfg.K2)
+    owner, cost = U.partition_lpt(gcfg.lengths, world, m, gcfg.d, gcfg.H)
+    ids = [i for i in range(len(gcfg.lengths)) if owner[i] == rank]
+    lengths = [gcfg.lengths[i] for i in ids]
+    x, dout = synth.layer_inputs(gcfg, ids=ids, lengths=lengths)
+    t = synth.timestamps(gcfg.seed, lengths, ids=ids)
+    pos, ts = synth.rab_tables(gcfg)
+    p = synth.layer_params(gcfg.d, gcfg.seed)
+    f = lambda a: torch.from_numpy(a).to(device)
+    b = lambda a: torch.from_numpy(a).to(device, torch.bfloat16)
+    prm = U.Params(f(p["ln1_w"]), f(p["ln1_b"]), b(p["w1"]), f(p["ln2_w"]), f(p["ln2_b"]), b(p["w2"]), f(p["b1"]),
+                   f(p["b2"]))
+    off = np.zeros(len(lengths) + 1, np.int32)
+    off[1:] = np.cumsum(lengths)
+    jag = U.JaggedBatch(off, device)
+    attn = U.Attn(gcfg.H, gcfg.dh, gcfg.alpha, float(gcfg.N), f(pos), f(ts), f(t))
+    return dict(cfg=gcfg, m=m, jag=jag, attn=attn, prm=prm, x_host=x, dout_host=dout, t_host=t, lengths=lengths,
+                rank_cost=cost, owner=owner)
+
+
+def grads_bucket(prm, attn, device):
+    """One flat fp32 buffer holding every parameter gradient (the all-reduce bucket)."""
+    import torch
+    shapes = [("ln1_w", prm.ln1_w), ("ln1_b", prm.ln1_b), ("w1", prm.w1), ("b1", prm.b1), ("ln2_w", prm.ln2_w),
+              ("ln2_b", prm.ln2_b), ("w2", prm.w2), ("b2", prm.b2), ("pos_bias", attn.pos_bias),
+              ("time_bias", attn.time_bias)]
+    n = sum(t.numel() for _, t in shapes if t is not None)
+    n = (n + 3) // 4 * 4 + 4 * len(shapes)
+    flat = torch.zeros(n, dtype=torch.float32, device=device)
+    views, off = {}, 0
+    for name, t in shapes:
+        if t is None:
+            views[name] = None
+            continue
+        views[name] = flat[off:off + t.numel()].view(t.shape)
+        off += (t.numel() + 3) // 4 * 4  # keep every view 16-byte aligned
+    return flat, views
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_16986_b200 import uhstu as U
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    W = setup_workload(args.config, world, rank, device)
+    cfg, m, jag, attn, prm = W["cfg"], W["m"], W["jag"], W["attn"], W["prm"]
+    T, d = jag.T, cfg.d
+    x = torch.from_numpy(W["x_host"]).to(device, torch.bfloat16)
+    dout = torch.from_numpy(W["dout_host"]).to(device, torch.bfloat16)
+    out = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    saved = U.alloc_saved(x)
+    flat, gviews = grads_bucket(prm, attn, device)
+    ws_f = U._ws(U.layer_workspace_bytes(jag, m, prm, attn, U.BF16, False), device)
+    ws_b = U._ws(U.layer_workspace_bytes(jag, m, prm, attn, U.BF16, True), device)
+
+    def step(xx, dd):
+        U.layer_fwd(jag, m, prm, attn, xx, out=out, ws=ws_f, saved=saved)
+        U.layer_bwd(jag, m, prm, attn, xx, saved, dd, grads=gviews, dx=dx, ws=ws_b)
+        if world > 1:
+            dist.all_reduce(flat)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(fn, K):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([ms], device=device)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step(x, dout)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    l0 = U.launch_count()
+    ms = timed(lambda: step(x, dout), args.steps)
+    launches = U.launch_count() - l0
+    clocks = sampler.stop() if sampler else None
+    ms_step = ms / args.steps
+    total_tokens = T * world if cfg.name == "cfg3" else sum(cfg.lengths)
+    value = total_tokens / (ms_step / 1e3)
+
+    # ---- attention alone (fwd, bwd) on the same batch, CUDA events on the launching stream
+    ok_rows = torch.empty(T, 4 * d, dtype=torch.bfloat16, device=device)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    sd = (4.0 / cfg.dh) ** 0.25
+    ok_rows.copy_((torch.randn(T, 4 * d, generator=g) * sd).to(torch.bfloat16))
+    q, k, v = ok_rows[:, 2 * d:3 * d], ok_rows[:, 3 * d:], ok_rows[:, d:2 * d]
+    dA = torch.randn(T, d, generator=g).to(device, torch.bfloat16)
+    A = torch.empty(T, d, dtype=torch.bfloat16, device=device)
+    gbuf = torch.empty(T, 3 * d, dtype=torch.bfloat16, device=device)
+    dq, dk, dv = gbuf[:, :d], gbuf[:, d:2 * d], gbuf[:, 2 * d:]
+    dpos, dts = torch.zeros_like(attn.pos_bias), torch.zeros_like(attn.time_bias)
+    wsa_f = U._ws(U.attn_workspace_bytes(jag, m, attn, U.BF16, False), device)
+    wsa_b = U._ws(U.attn_workspace_bytes(jag, m, attn, U.BF16, True), device)
+    fa = lambda: U.attn_fwd(jag, m, attn, q, k, v, out=A, ws=wsa_f)
+    fb = lambda: U.attn_bwd(jag, m, attn, q, k, v, dA, dq, dk, dv, dpos, dts, ws=wsa_b)
+    for _ in range(2):
+        fa(); fb()
+    fwd_ms = timed(fa, args.steps) / args.steps
+    bwd_ms = timed(fb, args.steps) / args.steps
+    nnz = U.batch_nnz(jag, m)
+    fwd_flop = 4.0 * cfg.dh * cfg.H * nnz
+    bwd_flop = 10.0 * cfg.dh * cfg.H * nnz
+    peaks = load_peaks()
+    attn_tflops = (fwd_flop + bwd_flop) / ((fwd_ms + bwd_ms) / 1e3) / 1e12
+
+    # ---- e2e through the public API from pinned host buffers (H2D inputs, D2H gradient bucket)
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(W["x_host"]).to(torch.bfloat16).pin_memory()
+        dh_ = torch.from_numpy(W["dout_host"]).to(torch.bfloat16).pin_memory()
+        th = torch.from_numpy(W["t_host"]).pin_memory()
+        gh = torch.empty(flat.numel(), dtype=torch.float32).pin_memory()
+        xd, dd = torch.empty_like(x), torch.empty_like(dout)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            dd.copy_(dh_, non_blocking=True)
+            attn.timestamps.copy_(th, non_blocking=True)
+            step(xd, dd)
+            gh.copy_(flat, non_blocking=True)
+
+        e2e_step()
+        e_ms = timed(e2e_step, args.steps) / args.steps
+        e2e = {"value": total_tokens / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(xh.numel() * 2 + dh_.numel() * 2 + th.numel() * 8),
+               "d2h_bytes_per_step": int(gh.numel() * 4)}
+
+    if rank != 0:
+        return None
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: ULTRA-HSTU layer fwd+bwd, {len(W['lengths'])} jagged seqs x L="
+                               f"{max(W['lengths'])} per GPU ({T} tokens), 4 heads x 128, SLA window {cfg.K1} + "
+                               f"{cfg.K2} global, rab (P={cfg.P}, NB={cfg.ts_len}), N={int(cfg.N)}",
+                   "global_batch_tokens": total_tokens, "seq_len": max(W["lengths"]),
+                   "parallelism": f"dp{world} (LPT token-balanced shards, NCCL all-reduce of the fp32 grad bucket)",
+                   "l2": "inputs larger than L2 (x 268 MB, step working set ~8 GB)"},
+        "attn": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "nnz_pairs_per_head": nnz,
+                 "effective_tflops": attn_tflops, "fwd_tflops": fwd_flop / (fwd_ms / 1e3) / 1e12,
+                 "bwd_tflops": bwd_flop / (bwd_ms / 1e3) / 1e12,
+                 "frac_of_measured_bf16_burst": attn_tflops / peaks["bf16_tflops"],
+                 "frac_of_datasheet_2250": attn_tflops / 2250.0,
+                 "flop_convention": "4*dh*H*nnz fwd + 10*dh*H*nnz bwd (unmasked pairs only)"},
+        "roofline": {"kernel": "attention fwd+bwd (attn_fwd_sm100, attn_bwd dq + dkv)", "bound": "tensor",
+                     "achieved": attn_tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": attn_tflops / peaks["bf16_tflops"], "peak_source": peaks["source"] + " (burst)",
+                     "traffic": None},
+        "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+        "clocks": clocks, "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
+    return line
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def oracle_sample(cfg, L: int):
+    """The oracle (as it stands) on one length-L sequence of the workload: layer fwd+bwd."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    from paper_2602_16986_b200 import synth
+    sub = synth.Config(cfg.name, [L], H=cfg.H, dh=cfg.dh, K1=cfg.K1, K2=cfg.K2, N=cfg.N, seed=cfg.seed,
+                       pos_len=cfg.P, ts_len=cfg.ts_len)
+    p = synth.layer_params(cfg.d, cfg.seed)
+    x, dout = synth.layer_inputs(sub)
+    pos, ts = synth.rab_tables(cfg)
+    t = synth.timestamps(cfg.seed, [L])
+    prm = O.LayerParams(**{k: np.asarray(v, np.float64) for k, v in p.items()})
+    spec = O.AttnSpec(K1=O.FULL if cfg.K1 >= synth.WINDOW_FULL else cfg.K1, K2=cfg.K2, alpha=cfg.alpha, N=cfg.N,
+                      pos_w=pos, ts_w=ts, timestamps=t)
+    t0 = time.perf_counter()
+    out, cache = O.layer_forward(x, sub.offsets(), prm, cfg.H, spec)
+    O.layer_backward(dout, sub.offsets(), prm, cfg.H, spec, cache=cache)
+    return time.perf_counter() - t0, O.num_threads()
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    L = 4096  # per-token attention work at L=4096 ~ L=16k under the 1024+128 window
+    dt, cores = oracle_sample(cfg, L)
+    return {"value": L / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"one {L}-token sequence of {cfg.name} (same dims/mask/rab), layer fwd+bwd, "
+                      f"fp64 C pair loops (OpenMP) + numpy GEMMs; {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from paper_2602_16986_b200 import synth
+    cfg = synth.config(args.config)
+    L = 2048
+    for _ in range(args.warmup):
+        oracle_sample(cfg, 256)
+    times = []
+    cores = 1
+    for _ in range(args.steps):
+        dt, cores = oracle_sample(cfg, L)
+        times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = L / (ms / 1e3)
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} (bounded sample: one {L}-token sequence per step)"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"one {L}-token sequence of {cfg.name} per step, layer fwd+bwd"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -81,7 +81,7 @@ constexpr int QT = 128 * 128 * 2;       // Q / dA tile bytes (2 x 16K blocks)
 constexpr int KT = 64 * 128 * 2;        // K / V tile bytes (2 x 8K blocks)
 constexpr int ST = 128 * 64 * 2;        // dS tile (1 block)
 constexpr int KV_STAGES = 3;
-constexpr int SMEM = 2 * QT + KV_STAGES * 2 * KT + 2 * ST + 1024 + 512;
+constexpr int SMEM = 2 * QT + KV_STAGES * 2 * KT + 2 * ST + 2 * kMaxPosSmem * 4 + 256 + 1024 + 512;
 
 struct __align__(8) Bars {
     uint64_t qa_full, qa_empty;
@@ -90,7 +90,6 @@ struct __align__(8) Bars {
     uint64_t ds_full[2], ds_empty[2];
     uint64_t dq_full, dq_empty;
     uint32_t tmem;
-    float dts[64];
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -103,7 +102,10 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
     uint8_t* sK = smem + 2 * QT;                      // [KV_STAGES]
     uint8_t* sV = sK + KV_STAGES * KT;                // [KV_STAGES]
     uint8_t* sdS = sV + KV_STAGES * KT;               // [2]
-    Bars* bars = reinterpret_cast<Bars*>(sdS + 2 * ST);
+    float* pos_s = reinterpret_cast<float*>(sdS + 2 * ST);
+    float* ts_s = pos_s + kMaxPosSmem;
+    float* dpos_s = ts_s + 64;                        // d pos_bias accumulator of this CTA
+    Bars* bars = reinterpret_cast<Bars*>(dpos_s + kMaxPosSmem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -116,7 +118,9 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         mbar_init(&bars->dq_full, 1); mbar_init(&bars->dq_empty, 8);
         fence_barrier_init();
     }
-    if (threadIdx.x < 64) bars->dts[threadIdx.x] = 0.f;
+    stage_rab(a, pos_s, ts_s);
+    if (a.dpos)
+        for (int i = threadIdx.x; i < a.P; i += blockDim.x) dpos_s[i] = 0.f;
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
@@ -213,6 +217,14 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         const int r = wq * 32 + lane;
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const int et = threadIdx.x - 128;  // 0..255 among epilogue threads
+        const float ha = 0.5f * a.alpha;
+        const float rscale = 0.5f * a.inv_n;   // ds = rscale * ds'  (ds' is what the kernel carries)
+        // d rab partials live in registers / thread-local memory / smem and reach global
+        // memory once per CTA (same-address global atomics from every row would serialise)
+        float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals), in ds' units
+        float ts_acc[32];          // d time_bias per bucket, this thread's rows
+#pragma unroll
+        for (int b = 0; b < 32; ++b) ts_acc[b] = 0.f;
         int sc = 0, dc = 0, qi = 0;
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
             const WorkItem it = a.items[w];
@@ -222,13 +234,18 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
             const int n = key_tiles_count(kt);
             const int qp = q0 + r;
             const bool qok = qp < L;
+            const ChunkCtx cx{a.pos ? pos_s : nullptr, a.P, a.ts ? ts_s : nullptr, a.NB, a.t ? a.t + o : nullptr,
+                              a.K1, a.K2, L, a.alpha};
             const int64_t tq = (a.ts && qok) ? __ldg(a.t + o + qp) : 0;
-            float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals)
-            int cur_b = -1;            // d time_bias run-length state
+            int cur_b = -1;            // d time_bias run-length state (buckets are monotone along the row)
             float cur_acc = 0.f;
+            int64_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
             for (int j = 0; j < n; ++j) {
                 const int k0 = key_tile_at(kt, j) * BN;
-                const int kbase = k0 + wg * 32;
+                const int kb = k0 + wg * 32;
+                const int64_t tcur = tnext;
+                if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
+                const QChunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -240,55 +257,54 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
                 ++sc;
-                // ---- bias (per 32-column chunk: constant fast path when possible)
-                const bool full_tile = qok && (kbase + 31 <= qp) && (qp - kbase <= a.K1 || kbase + 31 < a.K2);
-                float pos_c = 0.f, ts_c = 0.f;
-                bool pos_const = true, ts_const = true;
-                int b_hi = 0;
-                if (a.pos) {
-                    pos_const = qp - (kbase + 31) >= a.P - 1;
-                    if (pos_const) pos_c = __ldg(a.pos + a.P - 1);
-                }
-                if (a.ts) {
-                    const int kl = imin(kbase + 31, L - 1), kf = imin(kbase, L - 1);
-                    b_hi = time_bucket(tq - __ldg(a.t + o + kf), a.NB);
-                    const int b_lo = time_bucket(tq - __ldg(a.t + o + kl), a.NB);
-                    ts_const = full_tile && b_hi == b_lo;
-                    if (ts_const) ts_c = __ldg(a.ts + b_hi);
-                }
+                // ds' = dP (1 + t)(1 + h (1 - t)),  h = x/2, t = tanh(h)  ==  2 N ds
                 float ds[32];
-                float tile_sum = 0.f;
+                float tsum = 0.f;
+                if (ch.uni) {
+                    const float hb = 0.5f * ch.bias;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const int kp = kbase + c;
-                    const bool ok = full_tile || (qok && kp < L && mask_ok(qp, kp, a.K1, a.K2));
-                    float x = a.alpha * sv[c] + pos_c + ts_c;
-                    if (ok && (!pos_const || !ts_const)) {
-                        if (!pos_const) { int dd = qp - kp; x += __ldg(a.pos + (dd < a.P - 1 ? dd : a.P - 1)); }
-                        if (!ts_const) x += __ldg(a.ts + time_bucket(tq - __ldg(a.t + o + kp), a.NB));
+                    for (int c = 0; c < 32; ++c) {
+                        const float hx = fmaf(sv[c], ha, hb);
+                        const float th = tanh_approx(hx);
+                        const float wv = fmaf(hx, 1.0f - th, 1.0f);
+                        ds[c] = dp[c] * (1.0f + th) * wv;
+                        tsum += ds[c];
                     }
-                    const float sg = __frcp_rn(1.0f + __expf(-x));
-                    const float v = dp[c] * sg * (1.0f + x * (1.0f - sg)) * a.inv_n;
-                    ds[c] = ok ? v : 0.f;
-                    tile_sum += ds[c];
-                }
-                // ---- d time_bias: run-length over buckets (non-increasing along the row)
-                if (a.dts) {
-                    if (ts_const) {
-                        if (b_hi != cur_b) { if (cur_b >= 0) atomicAdd(&bars->dts[cur_b], cur_acc); cur_b = b_hi; cur_acc = 0.f; }
-                        cur_acc += tile_sum;
-                    } else {
-#pragma unroll 1
-                        for (int c = 0; c < 32; ++c) {
-                            if (ds[c] == 0.f) continue;
-                            const int b = time_bucket(tq - __ldg(a.t + o + kbase + c), a.NB);
-                            if (b != cur_b) { if (cur_b >= 0) atomicAdd(&bars->dts[cur_b], cur_acc); cur_b = b; cur_acc = 0.f; }
-                            cur_acc += ds[c];
+                    if (!qok) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) ds[c] = 0.f;
+                        tsum = 0.f;
+                    }
+                    if (a.dts && qok) {
+                        if (ch.b0 != cur_b) {
+                            if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
+                            cur_b = ch.b0; cur_acc = 0.f;
+                        }
+                        cur_acc += tsum;
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        float b;
+                        int bk;
+                        const bool ok = q_elem(cx, ch, qp, qok, tq, kb, c, b, bk);
+                        const float hx = fmaf(sv[c], ha, 0.5f * b);
+                        const float th = tanh_approx(hx);
+                        const float wv = fmaf(hx, 1.0f - th, 1.0f);
+                        const float v = ok ? dp[c] * (1.0f + th) * wv : 0.f;
+                        ds[c] = v;
+                        tsum += v;
+                        if (a.dts && ok) {
+                            if (bk != cur_b) {
+                                if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
+                                cur_b = bk; cur_acc = 0.f;
+                            }
+                            cur_acc += v;
                         }
                     }
                 }
-                far_acc += tile_sum;
-                // ---- dS (bf16) -> smem for dQ += dS K
+                far_acc += tsum;
+                // ---- dS' (bf16) -> smem for dQ += dS K
                 const int db = dc & 1;
                 mbar_wait(&bars->ds_empty[db], ((dc >> 1) & 1) ^ 1);
                 uint8_t* tile = sdS + db * ST;
@@ -297,34 +313,29 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_full[db]);
                 ++dc;
-                // ---- d pos_bias near diagonals (delta <= P-2) from the bf16 dS tile
+                // ---- d pos_bias near diagonals (delta <= P-2) from the bf16 dS' tile
                 if (a.dpos) {
                     const int D0 = q0 - k0;
                     const int lo = imax(0, D0 - (BN - 1)), hi = imin(a.P - 2, D0 + BM - 1);
                     if (lo <= hi) {
                         named_bar_sync(1, 256);
+                        // one owner thread per diagonal: no atomics, smem accumulator per CTA
                         const int nd = hi - lo + 1;
-                        for (int idx = et; idx < nd * 4; idx += 256) {
-                            const int delta = lo + (idx >> 2), part = idx & 3;
+                        for (int idx = et; idx < nd; idx += 256) {
+                            const int delta = lo + idx;
                             float sum = 0.f;
-                            // rows i with j = i + D0 - delta in [0, BN)
                             const int i0 = imax(0, delta - D0), i1 = imin(BM, delta - D0 + BN);
-                            for (int i = i0 + part; i < i1; i += 4) sum += load_bf16_sw(tile, i, i + D0 - delta);
-                            if (sum != 0.f) { atomicAdd(a.dpos + delta, sum); far_acc -= sum; }
+                            for (int i = i0; i < i1; ++i) sum += load_bf16_sw(tile, i, i + D0 - delta);
+                            dpos_s[delta] += sum;
+                            far_acc -= sum;
                         }
                         named_bar_sync(1, 256);
                     }
                 }
             }
-            // ---- flush rab partials of this item
-            if (a.dts && cur_b >= 0) atomicAdd(&bars->dts[cur_b], cur_acc);
-            if (a.dpos) {
-                float f = far_acc;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
-                if (lane == 0 && f != 0.f) atomicAdd(a.dpos + a.P - 1, f);
-            }
-            // ---- dQ epilogue
+            // ---- close this item's time-bucket run
+            if (a.dts && cur_b >= 0) ts_acc[cur_b] += cur_acc;
+            // ---- dQ epilogue: dQ = alpha/(2N) * (dS' K)
             mbar_wait(&bars->dq_full, qi & 1);
             tc_fence_after();
             float v[64];
@@ -334,11 +345,39 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->dq_empty);
-            if (qok) store_out_row64(a.dq, a.ld_grad, o + qp, h * DH + wg * 64, v, a.gq, a.ld_gate, a.alpha);
+            if (qok) store_out_row64(a.dq, a.ld_grad, o + qp, h * DH + wg * 64, v, a.gq, a.ld_gate, ha * a.inv_n);
+        }
+        // ---- CTA-level reduction of the d rab partials, then one global atomic per entry
+        if (a.dpos || a.dts) {
+            float* red = reinterpret_cast<float*>(sQ);          // Q/dA tiles are no longer in use
+            named_bar_sync(2, 256);
+            if (a.dts) {
+#pragma unroll
+                for (int b = 0; b < 32; ++b) red[b * 256 + et] = ts_acc[b];
+            }
+            float f = far_acc;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
+            if (lane == 0) red[32 * 256 + (et >> 5)] = f;
+            named_bar_sync(2, 256);
+            if (a.dts && et < a.NB) {
+                float sum = 0.f;
+                for (int i = 0; i < 256; ++i) sum += red[et * 256 + i];
+                if (sum != 0.f) atomicAdd(a.dts + et, sum * rscale);
+            }
+            if (a.dpos) {
+                if (et == 0) {
+                    float sum = 0.f;
+                    for (int i = 0; i < 8; ++i) sum += red[32 * 256 + i];
+                    dpos_s[a.P - 1] += sum;
+                }
+                named_bar_sync(2, 256);
+                for (int i = et; i < a.P; i += 256)
+                    if (dpos_s[i] != 0.f) atomicAdd(a.dpos + i, dpos_s[i] * rscale);
+            }
         }
     }
     __syncthreads();
-    if (a.dts && threadIdx.x < a.NB && bars->dts[threadIdx.x] != 0.f) atomicAdd(a.dts + threadIdx.x, bars->dts[threadIdx.x]);
     if (warp == 2) tmem_dealloc<512>(tmem);
 }
 }  // namespace dq
@@ -350,7 +389,7 @@ constexpr int KT = 128 * 128 * 2;         // K / V tile bytes
 constexpr int QT = 64 * 128 * 2;          // Q / dA tile bytes
 constexpr int PT = 128 * 64 * 2;          // P^T / dS^T tile bytes
 constexpr int QA_STAGES = 3;
-constexpr int SMEM = 2 * KT + QA_STAGES * 2 * QT + 2 * PT + 1024 + 512;
+constexpr int SMEM = 2 * KT + QA_STAGES * 2 * QT + 2 * PT + kMaxPosSmem * 4 + 256 + 1024 + 512;
 
 struct __align__(8) Bars {
     uint64_t kv_full, kv_empty;
@@ -378,7 +417,9 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
     uint8_t* sdA = sQ + QA_STAGES * QT;          // [QA_STAGES]
     uint8_t* sP = sdA + QA_STAGES * QT;
     uint8_t* sdS = sP + PT;
-    Bars* bars = reinterpret_cast<Bars*>(sdS + PT);
+    float* pos_s = reinterpret_cast<float*>(sdS + PT);
+    float* ts_s = pos_s + kMaxPosSmem;
+    Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -389,6 +430,7 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         mbar_init(&bars->acc_full, 1); mbar_init(&bars->acc_empty, 8);
         fence_barrier_init();
     }
+    stage_rab(a, pos_s, ts_s);
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
@@ -484,6 +526,7 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
         const int wg = (warp - 4) >> 2, wq = warp & 3;
         const int r = wq * 32 + lane;
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        const float ha = 0.5f * a.alpha;
         int sc = 0, pc = 0, ki = 0;
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
             const WorkItem it = a.items[w];
@@ -492,9 +535,15 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
             const int n = n_qtiles(k0, L, a.K1, a.K2);
             const int kp = k0 + r;
             const bool kok = kp < L;
+            const ChunkCtx cx{a.pos ? pos_s : nullptr, a.P, a.ts ? ts_s : nullptr, a.NB, a.t ? a.t + o : nullptr,
+                              a.K1, a.K2, L, a.alpha};
             const int64_t tk = (a.ts && kok) ? __ldg(a.t + o + kp) : 0;
+            int64_t tnext = col_time(cx, (k0 / BN) * BN + wg * 32, lane);
             for (int i = 0; i < n; ++i) {
-                const int qbase = (k0 / BN + i) * BN + wg * 32;
+                const int qb = (k0 / BN + i) * BN + wg * 32;
+                const int64_t tcur = tnext;
+                if (i + 1 < n) tnext = col_time(cx, (k0 / BN + i + 1) * BN + wg * 32, lane);
+                const QChunk ch = k_chunk(cx, kp, kok, tk, qb, lane, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -506,35 +555,29 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
                 ++sc;
-                // all 32 (q, kp) allowed?  q in [qbase, qbase+31]
-                const bool full_tile = kok && (qbase >= kp) && (qbase + 31 < L) &&
-                                       (qbase + 31 - kp <= a.K1 || kp < a.K2);
-                float pos_c = 0.f, ts_c = 0.f;
-                bool pos_const = true, ts_const = true;
-                if (a.pos) {
-                    pos_const = qbase - kp >= a.P - 1;
-                    if (pos_const) pos_c = __ldg(a.pos + a.P - 1);
-                }
-                if (a.ts) {
-                    const int ql = imin(qbase + 31, L - 1), qf = imin(qbase, L - 1);
-                    const int b_lo = time_bucket(__ldg(a.t + o + qf) - tk, a.NB);
-                    const int b_hi = time_bucket(__ldg(a.t + o + ql) - tk, a.NB);
-                    ts_const = full_tile && b_hi == b_lo;
-                    if (ts_const) ts_c = __ldg(a.ts + b_lo);
-                }
+                // p' = silu(x) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  h = x/2, t = tanh(h)
                 float p[32], ds[32];
+                if (ch.uni) {
+                    const float hb = 0.5f * ch.bias;
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const int qp = qbase + c;
-                    const bool ok = full_tile || (kok && qp < L && mask_ok(qp, kp, a.K1, a.K2));
-                    float x = a.alpha * sv[c] + pos_c + ts_c;
-                    if (ok && (!pos_const || !ts_const)) {
-                        if (!pos_const) { int dd = qp - kp; x += __ldg(a.pos + (dd < a.P - 1 ? dd : a.P - 1)); }
-                        if (!ts_const) x += __ldg(a.ts + time_bucket(__ldg(a.t + o + qp) - tk, a.NB));
+                    for (int c = 0; c < 32; ++c) {
+                        const float hx = fmaf(sv[c], ha, hb);
+                        const float th = tanh_approx(hx);
+                        const float a1 = 1.0f + th;
+                        p[c] = hx * a1;
+                        ds[c] = dp[c] * a1 * fmaf(hx, 1.0f - th, 1.0f);
                     }
-                    const float sg = __frcp_rn(1.0f + __expf(-x));
-                    p[c] = ok ? x * sg * a.inv_n : 0.f;
-                    ds[c] = ok ? a.alpha * dp[c] * sg * (1.0f + x * (1.0f - sg)) * a.inv_n : 0.f;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        float b;
+                        const bool ok = k_elem(cx, ch, kp, kok, tk, qb, c, b);
+                        const float hx = fmaf(sv[c], ha, 0.5f * b);
+                        const float th = tanh_approx(hx);
+                        const float a1 = 1.0f + th;
+                        p[c] = ok ? hx * a1 : 0.f;
+                        ds[c] = ok ? dp[c] * a1 * fmaf(hx, 1.0f - th, 1.0f) : 0.f;
+                    }
                 }
                 mbar_wait(&bars->p_empty, (pc & 1) ^ 1);
                 store_bf16_row32(sP, r, wg * 32, p);
@@ -556,8 +599,8 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->acc_empty);
             if (kok) {
-                store_out_row64(a.dv, a.ld_grad, o + kp, h * DH + wg * 64, dv, a.gv, a.ld_gate, 1.0f);
-                store_out_row64(a.dk, a.ld_grad, o + kp, h * DH + wg * 64, dk, a.gk, a.ld_gate, 1.0f);
+                store_out_row64(a.dv, a.ld_grad, o + kp, h * DH + wg * 64, dv, a.gv, a.ld_gate, a.inv_n);
+                store_out_row64(a.dk, a.ld_grad, o + kp, h * DH + wg * 64, dk, a.gk, a.ld_gate, ha * a.inv_n);
             }
         }
     }

@@ -81,4 +81,123 @@ UH_HD int query_end(int k0, int rows, int L, int K1, int K2) {
     return e < L ? (int)e : L;
 }
 
+// ----------------------------------------------------------------------------
+// 32-column chunks of a score tile, seen by one thread-row (tcgen05 epilogues).
+//
+// The epilogue budget is ~8 lane-ops per score element at full tensor rate, so
+// the mask and the rab bias are resolved per 32-column chunk: when every lane of
+// the warp has a fully visible chunk with a constant position bucket and a
+// constant time bucket (the common case away from the diagonal and the band
+// edge), the whole chunk takes the fast path "x = alpha*S + bias_lane".  Otherwise
+// the warp evaluates mask and bias per element.  rab tables live in smem
+// (pos_s: P floats, ts_s: NB floats).  Rows beyond L are "don't care" (their
+// outputs are never stored) and never force the slow path.
+// ----------------------------------------------------------------------------
+struct ChunkCtx {
+    const float* pos_s; int P;
+    const float* ts_s; int NB;
+    const int64_t* t;   // timestamps of this sequence (t + seq_start) or nullptr
+    int K1, K2, L;
+    float alpha;
+};
+
+UH_DEV int64_t shfl64(int64_t v, int src) {
+    int lo = __shfl_sync(0xffffffffu, (int)(v & 0xffffffff), src);
+    int hi = __shfl_sync(0xffffffffu, (int)(v >> 32), src);
+    return ((int64_t)hi << 32) | (uint32_t)lo;
+}
+
+// rows are queries (forward, dQ); columns are keys kb..kb+31
+struct QChunk {
+    bool uni;        // warp-uniform fast path
+    float bias;      // per-lane constant bias on the fast path
+    int b0;          // time bucket of the chunk's first column (constant on the fast path)
+    int64_t tcol;    // this lane's column timestamp (for the slow path)
+};
+// tcol: this lane's column timestamp t[col0 + lane] (prefetched one tile ahead by the caller)
+UH_DEV int64_t col_time(const ChunkCtx& c, int col0, int lane) {
+    return c.ts_s ? __ldg(c.t + imin(col0 + lane, c.L - 1)) : 0;
+}
+UH_DEV QChunk q_chunk(const ChunkCtx& c, int qp, bool qok, int64_t tq, int kb, int lane, int64_t tcol) {
+    QChunk r;
+    bool full = (kb + 31 <= qp) && (qp - kb <= c.K1 || kb + 31 < c.K2);
+    bool uni = full;
+    float bias = 0.f;
+    if (c.pos_s) {
+        uni = uni && (qp - kb - 31 >= c.P - 1);
+        bias += c.pos_s[c.P - 1];
+    }
+    r.tcol = 0;
+    r.b0 = 0;
+    if (c.ts_s) {
+        r.tcol = tcol;
+        const int b0 = time_bucket(tq - shfl64(r.tcol, 0), c.NB);
+        const int b1 = time_bucket(tq - shfl64(r.tcol, 31), c.NB);
+        uni = uni && b0 == b1;
+        bias += c.ts_s[b0];
+        r.b0 = b0;
+    }
+    r.uni = __all_sync(0xffffffffu, uni || !qok);
+    r.bias = bias;
+    return r;
+}
+// slow path for one element of a query-row chunk: returns false when masked
+UH_DEV bool q_elem(const ChunkCtx& c, const QChunk& ch, int qp, bool qok, int64_t tq, int kb, int j, float& bias,
+                   int& bkt) {
+    const int kp = kb + j;
+    const int64_t tk = c.ts_s ? shfl64(ch.tcol, j) : 0;
+    bias = 0.f;
+    bkt = 0;
+    if (c.pos_s) { int dd = qp - kp; dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1); bias += c.pos_s[dd]; }
+    if (c.ts_s) { bkt = time_bucket(tq - tk, c.NB); bias += c.ts_s[bkt]; }
+    return qok && kp < c.L && mask_ok(qp, kp, c.K1, c.K2);
+}
+UH_DEV bool q_elem(const ChunkCtx& c, const QChunk& ch, int qp, bool qok, int64_t tq, int kb, int j, float& bias) {
+    int b;
+    return q_elem(c, ch, qp, qok, tq, kb, j, bias, b);
+}
+
+// rows are keys (dK/dV); columns are queries qb..qb+31
+UH_DEV QChunk k_chunk(const ChunkCtx& c, int kp, bool kok, int64_t tk, int qb, int lane, int64_t tcol) {
+    QChunk r;
+    bool full = (qb >= kp) && (qb + 31 < c.L) && (qb + 31 - kp <= c.K1 || kp < c.K2);
+    bool uni = full;
+    float bias = 0.f;
+    if (c.pos_s) {
+        uni = uni && (qb - kp >= c.P - 1);
+        bias += c.pos_s[c.P - 1];
+    }
+    r.tcol = 0;
+    r.b0 = 0;
+    if (c.ts_s) {
+        r.tcol = tcol;
+        const int b0 = time_bucket(shfl64(r.tcol, 0) - tk, c.NB);
+        const int b1 = time_bucket(shfl64(r.tcol, 31) - tk, c.NB);
+        uni = uni && b0 == b1;
+        bias += c.ts_s[b0];
+        r.b0 = b0;
+    }
+    r.uni = __all_sync(0xffffffffu, uni || !kok);
+    r.bias = bias;
+    return r;
+}
+UH_DEV bool k_elem(const ChunkCtx& c, const QChunk& ch, int kp, bool kok, int64_t tk, int qb, int j, float& bias) {
+    const int qp = qb + j;
+    const int64_t tq = c.ts_s ? shfl64(ch.tcol, j) : 0;
+    bias = 0.f;
+    if (c.pos_s) { int dd = qp - kp; dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1); bias += c.pos_s[dd]; }
+    if (c.ts_s) bias += c.ts_s[time_bucket(tq - tk, c.NB)];
+    return kok && qp < c.L && mask_ok(qp, kp, c.K1, c.K2);
+}
+
+// Stage the rab tables into shared memory (all threads of the CTA; caller syncs).
+UH_DEV void stage_rab(const AttnArgs& a, float* pos_s, float* ts_s) {
+    if (a.pos)
+        for (int i = threadIdx.x; i < a.P; i += blockDim.x) pos_s[i] = __ldg(a.pos + i);
+    if (a.ts)
+        for (int i = threadIdx.x; i < a.NB; i += blockDim.x) ts_s[i] = __ldg(a.ts + i);
+}
+
+constexpr int kMaxPosSmem = 2048;  // bf16 tcgen05 path: pos_bias_len <= 2048 (validated)
+
 }  // namespace uh

@@ -127,12 +127,8 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     a.bias = g.bias; a.resid = (const __nv_bfloat16*)g.resid; a.ldr = g.ldr;
     const int total = a.m_tiles * a.n_tiles * a.k_splits;
     auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI>;
-    static bool attr_set = false;  // idempotent per instantiation
-    if (!attr_set) {
-        UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_set = true;
-    }
-    kern<<<std::min(total, sms), 256, C::SMEM, st>>>(ta, tb, a);
+    UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    kern<<<std::min(total, sms), 384, C::SMEM, st>>>(ta, tb, a);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;

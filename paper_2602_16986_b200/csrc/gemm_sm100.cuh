@@ -13,8 +13,9 @@
 //   EPI_SILU : h = acc + bias[n]; out0 = bf16(silu(h)); out1 = bf16(silu'(h))  f1 + phi1 (Eq. 2)
 //   EPI_F32  : atomically add acc into fp32 out0 (split-K weight gradients)
 //
-// Roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM
-// allocator, warps 4-7 epilogue (thread = TMEM lane = output row).  TMEM holds two
+// Roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2 TMEM
+// allocator, warps 4-11 epilogue in two warpgroups that split the BN columns
+// (thread = TMEM lane = output row).  TMEM holds two
 // BN-column accumulators so the epilogue of tile i overlaps the main loop of i+1.
 #pragma once
 #include "sm100.cuh"
@@ -44,7 +45,7 @@ struct GemmCfg {
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
     using C = GemmCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
@@ -62,7 +63,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
         fence_barrier_init();
     }
     if (warp == 0 && lane_id() == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
@@ -152,7 +153,8 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        const int wq = warp - 4;              // TMEM lane quarter
+        const int wq = warp & 3;              // TMEM lane quarter
+        const int wg = (warp - 4) >> 2;       // column half of the tile
         const int row_in_tile = wq * 32 + (int)lane_id();
         int it = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
@@ -164,7 +166,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             const int row = mt * C::BM + row_in_tile;
             const bool row_ok = row < g.M;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = wg * (BN / 2); c0 < (wg + 1) * (BN / 2); c0 += 32) {
                 float v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + c0, v);
                 tmem_ld_wait();
@@ -201,12 +203,14 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             op[j] = make_uint4(pack_bf16(v[j * 8 + 0], v[j * 8 + 1]), pack_bf16(v[j * 8 + 2], v[j * 8 + 3]),
                                                pack_bf16(v[j * 8 + 4], v[j * 8 + 5]), pack_bf16(v[j * 8 + 6], v[j * 8 + 7]));
                     } else {  // EPI_SILU
+                        // silu(v) = h (1 + t), silu'(v) = (1 + t)(1 + h (1 - t)) / 2, h = v/2, t = tanh(h)
                         float s[32], gp[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            float sg = 1.0f / (1.0f + __expf(-v[j]));
-                            s[j] = v[j] * sg;
-                            gp[j] = sg * (1.0f + v[j] * (1.0f - sg));
+                            const float hv = 0.5f * v[j];
+                            const float t = tanh_approx(hv);
+                            s[j] = fmaf(hv, t, hv);
+                            gp[j] = 0.5f * (1.0f + t) * fmaf(hv, 1.0f - t, 1.0f);
                         }
                         uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out0) + (int64_t)row * g.ld0 + col);
 #pragma unroll
@@ -224,7 +228,8 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&tempty[acc]);
         }
     }
     __syncthreads();

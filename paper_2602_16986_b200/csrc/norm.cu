@@ -324,15 +324,23 @@ __global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* _
 }
 
 // ------------------------------------------------------------------ column sums / scale
+// column sums: each thread owns one 16-byte column vector and walks a slice of rows
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_k(int64_t nrows, int n, const T* __restrict__ M, int64_t ldm,
                                                 int64_t rows_per_block, float* out) {
-    const int col = blockIdx.x * 256 + threadIdx.x;
-    if (col >= n) return;
+    constexpr int V = Vec<T>::N;
+    const int ch = blockIdx.x * 256 + threadIdx.x;
+    if (ch * V >= n) return;
     const int64_t r0 = blockIdx.y * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
-    float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) s += static_cast<float>(M[r * ldm + col]);
-    atomicAdd(out + col, s);
+    float s[V] = {};
+    for (int64_t r = r0; r < r1; ++r) {
+        float v[V];
+        Vec<T>::load(M + r * ldm + ch * V, v);
+#pragma unroll
+        for (int e = 0; e < V; ++e) s[e] += v[e];
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) atomicAdd(out + ch * V + e, s[e]);
 }
 
 template <typename T>
@@ -444,10 +452,11 @@ uh_status ln_bwd(uh_dtype dt, int64_t T_, int d, const void* dxh, int64_t ldg, c
 
 uh_status colsum(uh_dtype dt, int64_t T_, int n, const void* M, int64_t ldm, float* out, cudaStream_t st) {
     if (T_ == 0 || n == 0) return UH_OK;
-    const int64_t cols_blocks = (n + 255) / 256;
-    int64_t ry = (2 * num_sms() + cols_blocks - 1) / cols_blocks;
+    const int V = dt == UH_BF16 ? 8 : 4;
+    const int64_t cols_blocks = (n / V + 255) / 256;
+    int64_t ry = (8 * num_sms() + cols_blocks - 1) / cols_blocks;
     int64_t rpb = (T_ + ry - 1) / ry;
-    if (rpb < 64) rpb = 64;
+    if (rpb < 32) rpb = 32;
     ry = (T_ + rpb - 1) / rpb;
     dim3 grid((unsigned)cols_blocks, (unsigned)ry);
     UH_DT_DISPATCH(dt, colsum_k<T><<<grid, 256, 0, st>>>(T_, n, (const T*)M, ldm, rpb, out));

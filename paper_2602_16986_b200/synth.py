@@ -45,7 +45,7 @@ class Config:
     rab: bool = True
     alpha: float = 1.0
     n_layers: int = 1
-    pos_len: int = 0         # P (0 -> max length)
+    pos_len: int = 0         # P (0 -> N); perf configs use 128: exact offsets < 127, one shared bias beyond (R7)
     ts_len: int = 32         # NB
 
     @property
@@ -90,22 +90,24 @@ def config(name: str, world: int = 1) -> Config:
         return Config("tiny128", [17, 40, 64], H=2, dh=128, K1=16, K2=2, N=64, seed=0)
     if name == "cfg2":
         return Config("cfg2", lengths_uniform(2, 32, 1024, 4096), H=4, dh=128,
-                      K1=WINDOW_FULL, K2=0, N=4096, seed=2)
+                      K1=WINDOW_FULL, K2=0, N=4096, seed=2, pos_len=128)
     if name == "cfg3":
-        return Config("cfg3", [16384] * 16, H=4, dh=128, K1=1024, K2=128, N=16384, seed=3)
+        return Config("cfg3", [16384] * 16 * world, H=4, dh=128, K1=1024, K2=128, N=16384, seed=3, pos_len=128)
     if name == "cfg4":
         return Config("cfg4", lengths_loguniform_until(4, 512, 16384, world * 262144), H=4, dh=128,
-                      K1=1024, K2=128, N=16384, seed=4, n_layers=18)
+                      K1=1024, K2=128, N=16384, seed=4, n_layers=18, pos_len=128)
     raise KeyError(name)
 
 
 # ----------------------------------------------------------------------------
 # draws
 # ----------------------------------------------------------------------------
-def timestamps(seed: int, lengths) -> np.ndarray:
-    """Per sequence: t0 ~ U[1.6e9, 1.7e9] s, gaps floor(exp(U(0, ln 86400))) s."""
+def timestamps(seed: int, lengths, ids=None) -> np.ndarray:
+    """Per sequence: t0 ~ U[1.6e9, 1.7e9] s, gaps floor(exp(U(0, ln 86400))) s.
+    ``ids`` are the global sequence ids (default 0..B-1) that key each stream."""
     out = []
-    for i, L in enumerate(lengths):
+    ids = range(len(lengths)) if ids is None else ids
+    for i, L in zip(ids, lengths):
         r = _rng(seed, i, 0x7)
         t0 = int(r.integers(1_600_000_000, 1_700_000_000))
         gaps = np.floor(np.exp(r.uniform(0.0, np.log(86400.0), size=max(L - 1, 0)))).astype(np.int64)
@@ -113,24 +115,26 @@ def timestamps(seed: int, lengths) -> np.ndarray:
     return np.concatenate(out) if out else np.zeros(0, np.int64)
 
 
-def rows_normal(seed: int, lengths, width: int, std: float, tag: int) -> np.ndarray:
-    """[T, width] float32 N(0, std^2) rounded to bf16, drawn per sequence."""
+def rows_normal(seed: int, lengths, width: int, std: float, tag: int, ids=None) -> np.ndarray:
+    """[T, width] float32 N(0, std^2) rounded to bf16, drawn per sequence (stream (seed, id, tag))."""
     blocks = []
-    for i, L in enumerate(lengths):
+    ids = range(len(lengths)) if ids is None else ids
+    for i, L in zip(ids, lengths):
         r = _rng(seed, i, tag)
         blocks.append(r.standard_normal((L, width), dtype=np.float32) * np.float32(std))
     a = np.concatenate(blocks, axis=0) if blocks else np.zeros((0, width), np.float32)
     return round_bf16(a)
 
 
-def attn_inputs(cfg: Config, seed: Optional[int] = None):
+def attn_inputs(cfg: Config, seed: Optional[int] = None, ids=None, lengths=None):
     """Q, K ~ N(0, sqrt(4/dh)) elementwise (scores ~ N(0, 2^2)), V ~ N(0,1); bf16-exact."""
     s = cfg.seed if seed is None else seed
+    lengths = cfg.lengths if lengths is None else lengths
     sd = (4.0 / cfg.dh) ** 0.25
-    q = rows_normal(s, cfg.lengths, cfg.d, sd, 0x51)
-    k = rows_normal(s, cfg.lengths, cfg.d, sd, 0x52)
-    v = rows_normal(s, cfg.lengths, cfg.d, 1.0, 0x53)
-    dA = rows_normal(s, cfg.lengths, cfg.d, 1.0, 0x54)
+    q = rows_normal(s, lengths, cfg.d, sd, 0x51, ids)
+    k = rows_normal(s, lengths, cfg.d, sd, 0x52, ids)
+    v = rows_normal(s, lengths, cfg.d, 1.0, 0x53, ids)
+    dA = rows_normal(s, lengths, cfg.d, 1.0, 0x54, ids)
     return q, k, v, dA
 
 
@@ -161,9 +165,10 @@ def layer_params(d: int, seed: int, layer: int = 0, biases: bool = True):
     return p
 
 
-def layer_inputs(cfg: Config, seed: Optional[int] = None):
-    """x ~ N(0,1) and dOut ~ N(0,1), [T, d], bf16-exact."""
+def layer_inputs(cfg: Config, seed: Optional[int] = None, ids=None, lengths=None):
+    """x ~ N(0,1) and dOut ~ N(0,1), [T, d], bf16-exact (optionally a subset of sequences)."""
     s = cfg.seed if seed is None else seed
-    x = rows_normal(s, cfg.lengths, cfg.d, 1.0, 0x61)
-    dout = rows_normal(s, cfg.lengths, cfg.d, 1.0, 0x62)
+    lengths = cfg.lengths if lengths is None else lengths
+    x = rows_normal(s, lengths, cfg.d, 1.0, 0x61, ids)
+    dout = rows_normal(s, lengths, cfg.d, 1.0, 0x62, ids)
     return x, dout

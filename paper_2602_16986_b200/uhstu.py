@@ -287,14 +287,19 @@ def layer_workspace_bytes(jag, m, prm: Params, attn: Attn, dtype: int, backward:
     return int(n.value)
 
 
-def layer_fwd(jag, m, prm: Params, attn: Attn, x, save: bool = True, out=None, ws=None):
+def alloc_saved(x: torch.Tensor) -> Saved:
+    f = lambda: torch.empty(x.shape[0], dtype=torch.float32, device=x.device)
+    return Saved(torch.empty_like(x), f(), f(), f(), f())
+
+
+def layer_fwd(jag, m, prm: Params, attn: Attn, x, save: bool = True, out=None, ws=None, saved: Optional[Saved] = None):
+    """out = HSTU layer(x) (Eqs. 1-5); returns (out, saved) — saved is the remat set for layer_bwd."""
     dt = _dtype_code(x)
-    T, d = x.shape
     out = torch.empty_like(x) if out is None else out
-    saved = None
-    if save:
-        f = lambda: torch.empty(T, dtype=torch.float32, device=x.device)
-        saved = Saved(torch.empty_like(x), f(), f(), f(), f())
+    if save and saved is None:
+        saved = alloc_saved(x)
+    if not save:
+        saved = None
     p = prm.c(attn)
     if ws is None:
         ws = _ws(layer_workspace_bytes(jag, m, prm, attn, dt, False), x.device)

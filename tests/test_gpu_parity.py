@@ -102,7 +102,7 @@ def test_attn_fwd_no_rab_alpha():
 
 def test_attn_fwd_cfg2_like_full_causal():
     lengths = synth.lengths_uniform(2, 6, 1024, 2048)
-    case = AttnCase(lengths, H=4, dh=128, K1=synth.WINDOW_FULL, K2=0, N=4096.0, seed=2)
+    case = AttnCase(lengths, H=4, dh=128, K1=synth.WINDOW_FULL, K2=0, N=4096.0, seed=2, P=128)
     assert rel_inf(run_fwd(case, U.BF16), oracle_fwd(case)) <= TOL[U.BF16]
 
 
