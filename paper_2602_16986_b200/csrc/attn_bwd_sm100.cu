@@ -93,7 +93,7 @@ struct __align__(8) Bars {
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -245,7 +245,7 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 const int kb = k0 + wg * 32;
                 const int64_t tcur = tnext;
                 if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
-                const QChunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
+                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -259,48 +259,47 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 ++sc;
                 // ds' = dP (1 + t)(1 + h (1 - t)),  h = x/2, t = tanh(h)  ==  2 N ds
                 float ds[32];
+                bool oth[32];
+                int bk[32];
+                q_bias<true>(cx, ch, qp, tq, kb, sv, ds, oth, bk);
                 float tsum = 0.f;
-                if (ch.uni) {
-                    const float hb = 0.5f * ch.bias;
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const float hx = fmaf(sv[c], ha, hb);
-                        const float th = tanh_approx(hx);
-                        const float wv = fmaf(hx, 1.0f - th, 1.0f);
-                        ds[c] = dp[c] * (1.0f + th) * wv;
-                        tsum += ds[c];
-                    }
-                    if (!qok) {
+                for (int c = 0; c < 32; ++c) {
+                    const float hx = 0.5f * ds[c];
+                    const float th = tanh_approx(hx);
+                    ds[c] = dp[c] * (1.0f + th) * fmaf(hx, 1.0f - th, 1.0f);
+                }
+                if (ch.m) {
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) ds[c] = 0.f;
-                        tsum = 0.f;
-                    }
-                    if (a.dts && qok) {
-                        if (ch.b0 != cur_b) {
+                    for (int c = 0; c < 32; ++c)
+                        if (!q_visible(cx, qp, qok, kb + c)) ds[c] = 0.f;
+                }
+                if (!qok) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) ds[c] = 0.f;
+                }
+#pragma unroll
+                for (int c = 0; c < 32; ++c) tsum += ds[c];
+                // d time_bias: run-length over buckets (non-increasing along the row)
+                if (a.dts && qok) {
+                    auto run_add = [&](int bb, float v) {
+                        if (bb != cur_b) {
                             if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
-                            cur_b = ch.b0; cur_acc = 0.f;
+                            cur_b = bb; cur_acc = 0.f;
                         }
-                        cur_acc += tsum;
-                    }
-                } else {
+                        cur_acc += v;
+                    };
+                    if (ch.tmode == 0) {
+                        run_add(ch.b_base, tsum);
+                    } else if (ch.tmode == 1) {
+                        float so = 0.f;
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        float b;
-                        int bk;
-                        const bool ok = q_elem(cx, ch, qp, qok, tq, kb, c, b, bk);
-                        const float hx = fmaf(sv[c], ha, 0.5f * b);
-                        const float th = tanh_approx(hx);
-                        const float wv = fmaf(hx, 1.0f - th, 1.0f);
-                        const float v = ok ? dp[c] * (1.0f + th) * wv : 0.f;
-                        ds[c] = v;
-                        tsum += v;
-                        if (a.dts && ok) {
-                            if (bk != cur_b) {
-                                if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
-                                cur_b = bk; cur_acc = 0.f;
-                            }
-                            cur_acc += v;
-                        }
+                        for (int c = 0; c < 32; ++c) so += oth[c] ? ds[c] : 0.f;
+                        run_add(ch.b_other, so);
+                        run_add(ch.b_base, tsum - so);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) run_add(bk[c], ds[c]);
                     }
                 }
                 far_acc += tsum;
@@ -407,7 +406,7 @@ __device__ __forceinline__ int n_qtiles(int k0, int L, int K1, int K2) {
 }
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -543,7 +542,7 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 const int qb = (k0 / BN + i) * BN + wg * 32;
                 const int64_t tcur = tnext;
                 if (i + 1 < n) tnext = col_time(cx, (k0 / BN + i + 1) * BN + wg * 32, lane);
-                const QChunk ch = k_chunk(cx, kp, kok, tk, qb, lane, tcur);
+                const Chunk ch = k_chunk(cx, kp, kok, tk, qb, lane, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -557,27 +556,19 @@ kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensor
                 ++sc;
                 // p' = silu(x) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  h = x/2, t = tanh(h)
                 float p[32], ds[32];
-                if (ch.uni) {
-                    const float hb = 0.5f * ch.bias;
+                k_bias(cx, ch, kp, tk, qb, sv, p);
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const float hx = fmaf(sv[c], ha, hb);
-                        const float th = tanh_approx(hx);
-                        const float a1 = 1.0f + th;
-                        p[c] = hx * a1;
-                        ds[c] = dp[c] * a1 * fmaf(hx, 1.0f - th, 1.0f);
-                    }
-                } else {
+                for (int c = 0; c < 32; ++c) {
+                    const float hx = 0.5f * p[c];
+                    const float th = tanh_approx(hx);
+                    const float a1 = 1.0f + th;
+                    p[c] = hx * a1;
+                    ds[c] = dp[c] * a1 * fmaf(hx, 1.0f - th, 1.0f);
+                }
+                if (ch.m) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        float b;
-                        const bool ok = k_elem(cx, ch, kp, kok, tk, qb, c, b);
-                        const float hx = fmaf(sv[c], ha, 0.5f * b);
-                        const float th = tanh_approx(hx);
-                        const float a1 = 1.0f + th;
-                        p[c] = ok ? hx * a1 : 0.f;
-                        ds[c] = ok ? dp[c] * a1 * fmaf(hx, 1.0f - th, 1.0f) : 0.f;
-                    }
+                    for (int c = 0; c < 32; ++c)
+                        if (!k_visible(cx, kp, kok, qb + c)) { p[c] = 0.f; ds[c] = 0.f; }
                 }
                 mbar_wait(&bars->p_empty, (pc & 1) ^ 1);
                 store_bf16_row32(sP, r, wg * 32, p);
@@ -620,9 +611,9 @@ uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStr
     UH_TRY(make_tmap_bf16(&dA128, aq.dout, width, T, aq.ld_dout, 64, 128));
     UH_TRY(make_tmap_bf16(&k64, aq.k, width, T, aq.ld_qkv, 64, 64));
     UH_TRY(make_tmap_bf16(&v64, aq.v, width, T, aq.ld_qkv, 64, 64));
-    UH_CUDA(cudaFuncSetAttribute(dq::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dq::SMEM));
+    UH_CUDA(cudaFuncSetAttribute(dq::attn_bwd_dq_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, dq::SMEM));
     const int sms = num_sms();
-    dq::kernel<<<aq.n_items < sms ? aq.n_items : sms, NUM_THREADS, dq::SMEM, st>>>(q128, k64, v64, dA128, aq);
+    dq::attn_bwd_dq_sm100<<<aq.n_items < sms ? aq.n_items : sms, NUM_THREADS, dq::SMEM, st>>>(q128, k64, v64, dA128, aq);
     note_launch();
     UH_CUDA(cudaGetLastError());
 
@@ -631,8 +622,8 @@ uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStr
     UH_TRY(make_tmap_bf16(&dA64, akv.dout, width, T, akv.ld_dout, 64, 64));
     UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));
     UH_TRY(make_tmap_bf16(&v128, akv.v, width, T, akv.ld_qkv, 64, 128));
-    UH_CUDA(cudaFuncSetAttribute(dkv::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv::SMEM));
-    dkv::kernel<<<akv.n_items < sms ? akv.n_items : sms, NUM_THREADS, dkv::SMEM, st>>>(q64, k128, v128, dA64, akv);
+    UH_CUDA(cudaFuncSetAttribute(dkv::attn_bwd_dkv_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv::SMEM));
+    dkv::attn_bwd_dkv_sm100<<<akv.n_items < sms ? akv.n_items : sms, NUM_THREADS, dkv::SMEM, st>>>(q64, k128, v128, dA64, akv);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;

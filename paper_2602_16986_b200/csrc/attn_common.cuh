@@ -85,13 +85,21 @@ UH_HD int query_end(int k0, int rows, int L, int K1, int K2) {
 // 32-column chunks of a score tile, seen by one thread-row (tcgen05 epilogues).
 //
 // The epilogue budget is ~8 lane-ops per score element at full tensor rate, so
-// the mask and the rab bias are resolved per 32-column chunk: when every lane of
-// the warp has a fully visible chunk with a constant position bucket and a
-// constant time bucket (the common case away from the diagonal and the band
-// edge), the whole chunk takes the fast path "x = alpha*S + bias_lane".  Otherwise
-// the warp evaluates mask and bias per element.  rab tables live in smem
-// (pos_s: P floats, ts_s: NB floats).  Rows beyond L are "don't care" (their
-// outputs are never stored) and never force the slow path.
+// the mask and the rab bias are resolved per 32-column chunk and every
+// per-element component is switched on only when some lane of the warp needs it
+// (warp-uniform flags, so no divergence):
+//   m     per-element mask (the chunk crosses the diagonal, the band edge, or L)
+//   pp    per-element position bias (the chunk is within P-1 of the diagonal)
+//   tmode 0: the time bucket is constant along every lane's chunk
+//         1: at most two buckets per lane -> one threshold compare per element
+//         2: generic per-element bucket (only right next to the diagonal)
+// Buckets of floor(log2 dt) are monotone along a row because timestamps are
+// sorted, so a lane's chunk has buckets b_first..b_last and "two buckets" means
+// one threshold on the column timestamp.  rab tables live in smem (pos_s: P
+// floats, ts_s: NB <= 32 floats).  Rows beyond L are "don't care" (their outputs
+// are never stored) and never force a per-element component.
+// Column timestamps are carried per lane as 32-bit offsets from the chunk's
+// first column (chunks must span < 2^31 s).
 // ----------------------------------------------------------------------------
 struct ChunkCtx {
     const float* pos_s; int P;
@@ -107,88 +115,157 @@ UH_DEV int64_t shfl64(int64_t v, int src) {
     return ((int64_t)hi << 32) | (uint32_t)lo;
 }
 
-// rows are queries (forward, dQ); columns are keys kb..kb+31
-struct QChunk {
-    bool uni;        // warp-uniform fast path
-    float bias;      // per-lane constant bias on the fast path
-    int b0;          // time bucket of the chunk's first column (constant on the fast path)
-    int64_t tcol;    // this lane's column timestamp (for the slow path)
-};
+UH_DEV int32_t clamp_i32(int64_t v) {
+    return (int32_t)(v < -1 ? -1 : (v > 0x7fffffffLL ? 0x7fffffffLL : v));
+}
+
 // tcol: this lane's column timestamp t[col0 + lane] (prefetched one tile ahead by the caller)
 UH_DEV int64_t col_time(const ChunkCtx& c, int col0, int lane) {
     return c.ts_s ? __ldg(c.t + imin(col0 + lane, c.L - 1)) : 0;
 }
-UH_DEV QChunk q_chunk(const ChunkCtx& c, int qp, bool qok, int64_t tq, int kb, int lane, int64_t tcol) {
-    QChunk r;
-    bool full = (kb + 31 <= qp) && (qp - kb <= c.K1 || kb + 31 < c.K2);
-    bool uni = full;
+
+struct Chunk {
+    bool m, pp;       // warp-uniform: per-element mask / position bias needed
+    int tmode;        // warp-uniform: 0 constant bucket, 1 threshold, 2 generic
+    float bias;       // per lane: constant part of the bias (pos[P-1] and ts[b_base])
+    float tdelta;     // per lane (tmode 1): ts[b_other] - ts[b_base]
+    int32_t thr;      // per lane (tmode 1): column offset threshold of the b_other side
+    int32_t rel;      // per lane: this lane's column timestamp - chunk base
+    int b_base, b_other;
+    int64_t tcol;     // per lane: column timestamp (tmode 2)
+};
+
+// rows are queries (forward, dQ); columns are keys kb..kb+31 (dt decreasing along the row)
+UH_DEV Chunk q_chunk(const ChunkCtx& c, int qp, bool qok, int64_t tq, int kb, int lane, int64_t tcol) {
+    Chunk r;
+    const bool full = (kb + 31 <= qp) && (qp - kb <= c.K1 || kb + 31 < c.K2);
+    bool pp = false;
     float bias = 0.f;
     if (c.pos_s) {
-        uni = uni && (qp - kb - 31 >= c.P - 1);
+        pp = qp - kb - 31 < c.P - 1;
         bias += c.pos_s[c.P - 1];
     }
-    r.tcol = 0;
-    r.b0 = 0;
+    int tm = 0;
+    r.tdelta = 0.f; r.thr = -1; r.rel = 0; r.b_base = 0; r.b_other = 0; r.tcol = tcol;
     if (c.ts_s) {
-        r.tcol = tcol;
-        const int b0 = time_bucket(tq - shfl64(r.tcol, 0), c.NB);
-        const int b1 = time_bucket(tq - shfl64(r.tcol, 31), c.NB);
-        uni = uni && b0 == b1;
-        bias += c.ts_s[b0];
-        r.b0 = b0;
+        const int64_t base = shfl64(tcol, 0);
+        const int bf = time_bucket(tq - base, c.NB);                 // first column: largest dt
+        const int bl = time_bucket(tq - shfl64(tcol, 31), c.NB);     // last column: smallest dt
+        r.b_base = bl; r.b_other = bf;
+        r.rel = clamp_i32(tcol - base);
+        tm = bf == bl ? 0 : (bf == bl + 1 ? 1 : 2);
+        if (tm == 1) {
+            r.tdelta = c.ts_s[bf] - c.ts_s[bl];
+            r.thr = clamp_i32(tq - (int64_t(1) << bf) - base);     // column in b_other iff rel <= thr
+        }
+        bias += c.ts_s[bl];
     }
-    r.uni = __all_sync(0xffffffffu, uni || !qok);
+    r.m = __any_sync(0xffffffffu, qok && !full);
+    r.pp = __any_sync(0xffffffffu, qok && pp);
+    const int t1 = __any_sync(0xffffffffu, qok && tm >= 1), t2 = __any_sync(0xffffffffu, qok && tm == 2);
+    r.tmode = t2 ? 2 : (t1 ? 1 : 0);
     r.bias = bias;
     return r;
-}
-// slow path for one element of a query-row chunk: returns false when masked
-UH_DEV bool q_elem(const ChunkCtx& c, const QChunk& ch, int qp, bool qok, int64_t tq, int kb, int j, float& bias,
-                   int& bkt) {
-    const int kp = kb + j;
-    const int64_t tk = c.ts_s ? shfl64(ch.tcol, j) : 0;
-    bias = 0.f;
-    bkt = 0;
-    if (c.pos_s) { int dd = qp - kp; dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1); bias += c.pos_s[dd]; }
-    if (c.ts_s) { bkt = time_bucket(tq - tk, c.NB); bias += c.ts_s[bkt]; }
-    return qok && kp < c.L && mask_ok(qp, kp, c.K1, c.K2);
-}
-UH_DEV bool q_elem(const ChunkCtx& c, const QChunk& ch, int qp, bool qok, int64_t tq, int kb, int j, float& bias) {
-    int b;
-    return q_elem(c, ch, qp, qok, tq, kb, j, bias, b);
 }
 
-// rows are keys (dK/dV); columns are queries qb..qb+31
-UH_DEV QChunk k_chunk(const ChunkCtx& c, int kp, bool kok, int64_t tk, int qb, int lane, int64_t tcol) {
-    QChunk r;
-    bool full = (qb >= kp) && (qb + 31 < c.L) && (qb + 31 - kp <= c.K1 || kp < c.K2);
-    bool uni = full;
+// rows are keys (dK/dV); columns are queries qb..qb+31 (dt increasing along the row)
+UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int64_t tk, int qb, int lane, int64_t tcol) {
+    Chunk r;
+    const bool full = (qb >= kp) && (qb + 31 < c.L) && (qb + 31 - kp <= c.K1 || kp < c.K2);
+    bool pp = false;
     float bias = 0.f;
     if (c.pos_s) {
-        uni = uni && (qb - kp >= c.P - 1);
+        pp = qb - kp < c.P - 1;
         bias += c.pos_s[c.P - 1];
     }
-    r.tcol = 0;
-    r.b0 = 0;
+    int tm = 0;
+    r.tdelta = 0.f; r.thr = 0x7fffffff; r.rel = 0; r.b_base = 0; r.b_other = 0; r.tcol = tcol;
     if (c.ts_s) {
-        r.tcol = tcol;
-        const int b0 = time_bucket(shfl64(r.tcol, 0) - tk, c.NB);
-        const int b1 = time_bucket(shfl64(r.tcol, 31) - tk, c.NB);
-        uni = uni && b0 == b1;
-        bias += c.ts_s[b0];
-        r.b0 = b0;
+        const int64_t base = shfl64(tcol, 0);
+        const int bf = time_bucket(base - tk, c.NB);                 // first column: smallest dt
+        const int bl = time_bucket(shfl64(tcol, 31) - tk, c.NB);     // last column: largest dt
+        r.b_base = bf; r.b_other = bl;
+        r.rel = clamp_i32(tcol - base);
+        tm = bf == bl ? 0 : (bl == bf + 1 ? 1 : 2);
+        if (tm == 1) {
+            r.tdelta = c.ts_s[bl] - c.ts_s[bf];
+            r.thr = clamp_i32(tk + (int64_t(1) << bl) - base);     // column in b_other iff rel >= thr
+        }
+        bias += c.ts_s[bf];
     }
-    r.uni = __all_sync(0xffffffffu, uni || !kok);
+    r.m = __any_sync(0xffffffffu, kok && !full);
+    r.pp = __any_sync(0xffffffffu, kok && pp);
+    const int t1 = __any_sync(0xffffffffu, kok && tm >= 1), t2 = __any_sync(0xffffffffu, kok && tm == 2);
+    r.tmode = t2 ? 2 : (t1 ? 1 : 0);
     r.bias = bias;
     return r;
 }
-UH_DEV bool k_elem(const ChunkCtx& c, const QChunk& ch, int kp, bool kok, int64_t tk, int qb, int j, float& bias) {
-    const int qp = qb + j;
-    const int64_t tq = c.ts_s ? shfl64(ch.tcol, j) : 0;
-    bias = 0.f;
-    if (c.pos_s) { int dd = qp - kp; dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1); bias += c.pos_s[dd]; }
-    if (c.ts_s) bias += c.ts_s[time_bucket(tq - tk, c.NB)];
+
+// x[c] = alpha * s[c] + rab(c) for a query-row chunk; returns the per-element bucket
+// in bk[] only when tmode == 2 (else bk is untouched).  Masking is separate (q_mask).
+template <bool WANT_BUCKET>
+UH_DEV void q_bias(const ChunkCtx& c, const Chunk& ch, int qp, int64_t tq, int kb, const float* s, float* x,
+                   bool* other, int* bk) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fmaf(s[j], c.alpha, ch.bias);
+    if (ch.pp) {
+        const float pl = c.pos_s[c.P - 1];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            int dd = qp - kb - j;
+            dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1);
+            x[j] += c.pos_s[dd] - pl;
+        }
+    }
+    if (ch.tmode == 1) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const bool o = __shfl_sync(0xffffffffu, ch.rel, j) <= ch.thr;
+            if (WANT_BUCKET) other[j] = o;
+            x[j] += o ? ch.tdelta : 0.f;
+        }
+    } else if (ch.tmode == 2) {
+        const float tb = c.ts_s[ch.b_base];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int b = time_bucket(tq - shfl64(ch.tcol, j), c.NB);
+            if (WANT_BUCKET) bk[j] = b;
+            x[j] += c.ts_s[b] - tb;
+        }
+    }
+}
+
+// the same for a key-row chunk (columns are queries)
+UH_DEV void k_bias(const ChunkCtx& c, const Chunk& ch, int kp, int64_t tk, int qb, const float* s, float* x) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fmaf(s[j], c.alpha, ch.bias);
+    if (ch.pp) {
+        const float pl = c.pos_s[c.P - 1];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            int dd = qb + j - kp;
+            dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1);
+            x[j] += c.pos_s[dd] - pl;
+        }
+    }
+    if (ch.tmode == 1) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] += (__shfl_sync(0xffffffffu, ch.rel, j) >= ch.thr) ? ch.tdelta : 0.f;
+    } else if (ch.tmode == 2) {
+        const float tb = c.ts_s[ch.b_base];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] += c.ts_s[time_bucket(shfl64(ch.tcol, j) - tk, c.NB)] - tb;
+    }
+}
+
+// per-element visibility (only called when ch.m)
+UH_DEV bool q_visible(const ChunkCtx& c, int qp, bool qok, int kp) {
+    return qok && kp < c.L && mask_ok(qp, kp, c.K1, c.K2);
+}
+UH_DEV bool k_visible(const ChunkCtx& c, int kp, bool kok, int qp) {
     return kok && qp < c.L && mask_ok(qp, kp, c.K1, c.K2);
 }
+
 
 // Stage the rab tables into shared memory (all threads of the CTA; caller syncs).
 UH_DEV void stage_rab(const AttnArgs& a, float* pos_s, float* ts_s) {

@@ -197,7 +197,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const int kb = key_tile_at(kt, j) * BN + wg * 32;
                 const int64_t tcur = tnext;
                 if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
-                const QChunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
+                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -208,22 +208,18 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
                 ++sc;
-                // silu(x) = h + h tanh(h), h = x/2, x = alpha S + bias
-                if (ch.uni) {
-                    const float hb = 0.5f * ch.bias;
+                // x = alpha S + rab;  silu(x) = h + h tanh(h), h = x/2
+                float x[32];
+                q_bias<false>(cx, ch, qp, tq, kb, s, x, nullptr, nullptr);
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        const float hx = fmaf(s[c], ha, hb);
-                        s[c] = fmaf(hx, tanh_approx(hx), hx);
-                    }
-                } else {
+                for (int c = 0; c < 32; ++c) {
+                    const float hx = 0.5f * x[c];
+                    s[c] = fmaf(hx, tanh_approx(hx), hx);
+                }
+                if (ch.m) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) {
-                        float b;
-                        const bool ok = q_elem(cx, ch, qp, qok, tq, kb, c, b);
-                        const float hx = fmaf(s[c], ha, 0.5f * b);
-                        s[c] = ok ? fmaf(hx, tanh_approx(hx), hx) : 0.0f;
-                    }
+                    for (int c = 0; c < 32; ++c)
+                        if (!q_visible(cx, qp, qok, kb + c)) s[c] = 0.0f;
                 }
                 const int pb = pc & 1;
                 mbar_wait(&bars->p_empty[pb], ((pc >> 1) & 1) ^ 1);

@@ -37,23 +37,24 @@ UH_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase
+// completes (or ~1 ms passes) instead of spinning and stealing issue slots.
 UH_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+        : "=r"(ok) : "r"(addr), "r"(parity), "r"(1000000u) : "memory");
     return ok != 0;
 }
-// Blocking wait on the phase with the given parity.  A wait that exceeds ~20 s
-// traps (turns a pipeline deadlock into a reported launch failure, not a hang).
+// Blocking wait on the phase with the given parity.  A wait that never completes
+// traps after ~20 s of suspended retries (a deadlock becomes a launch error, not a hang).
 UH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
-    if (mbar_try_wait(addr, parity)) return;
-    const long long t0 = clock64();
+    uint32_t n = 0;
     while (!mbar_try_wait(addr, parity)) {
-        if (clock64() - t0 > 40000000000LL) __trap();
+        if (++n > 20000u) __trap();
     }
 }
 

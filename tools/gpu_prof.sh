@@ -4,6 +4,6 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -3
 timeout 300 python tools/prof_layer.py 2 2 > gpurun_out/prof_plain.log 2>&1 && \
 timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:"attn_fwd|dq|dkv" -s 3 -c 3 -o gpurun_out/prof_full \
+    -k regex:"attn_" -s 3 -c 3 -o gpurun_out/prof_full \
     python tools/prof_layer.py 2 2 > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?"; tail -5 gpurun_out/ncu_full.log
