@@ -106,7 +106,8 @@ typedef struct {
  * norm_n is the 1/N normaliser (R5), alpha the score scale (R6).
  * head_dim in {32, 64, 128} (bf16 tcgen05 kernels require 128; 32/64 run the
  * fp32 verification build only).  time_bias_len <= 32 (buckets of log2 seconds);
- * the bf16 path stages pos_bias in shared memory and requires pos_bias_len <= 2048.
+ * the bf16 path keeps pos_bias in shared memory / registers and requires
+ * pos_bias_len <= 256 (exact relative offsets up to 255, one shared bias beyond).
  * ------------------------------------------------------------------------- */
 typedef struct {
     int32_t num_heads;

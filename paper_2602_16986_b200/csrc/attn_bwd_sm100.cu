@@ -81,7 +81,7 @@ constexpr int QT = 128 * 128 * 2;       // Q / dA tile bytes (2 x 16K blocks)
 constexpr int KT = 64 * 128 * 2;        // K / V tile bytes (2 x 8K blocks)
 constexpr int ST = 128 * 64 * 2;        // dS tile (1 block)
 constexpr int KV_STAGES = 3;
-constexpr int SMEM = 2 * QT + KV_STAGES * 2 * KT + 2 * ST + 2 * kMaxPosSmem * 4 + 256 + 1024 + 512;
+constexpr int SMEM = 2 * QT + KV_STAGES * 2 * KT + 2 * ST + kPosTab * 4 + 256 + 1024 + 512;
 
 struct __align__(8) Bars {
     uint64_t qa_full, qa_empty;
@@ -103,9 +103,8 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     uint8_t* sV = sK + KV_STAGES * KT;                // [KV_STAGES]
     uint8_t* sdS = sV + KV_STAGES * KT;               // [2]
     float* pos_s = reinterpret_cast<float*>(sdS + 2 * ST);
-    float* ts_s = pos_s + kMaxPosSmem;
-    float* dpos_s = ts_s + 64;                        // d pos_bias accumulator of this CTA
-    Bars* bars = reinterpret_cast<Bars*>(dpos_s + kMaxPosSmem);
+    float* ts_s = pos_s + kPosTab;
+    Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -119,8 +118,6 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
-    if (a.dpos)
-        for (int i = threadIdx.x; i < a.P; i += blockDim.x) dpos_s[i] = 0.f;
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
@@ -222,6 +219,11 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         // d rab partials live in registers / thread-local memory / smem and reach global
         // memory once per CTA (same-address global atomics from every row would serialise)
         float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals), in ds' units
+        // near diagonals: tile offsets are multiples of 32, so this lane only ever meets
+        // diagonals lane + 32 t; their partial sums stay in registers (P <= 256 -> t < 8)
+        float dpr[kMaxNearT];
+#pragma unroll
+        for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
         float ts_acc[32];          // d time_bias per bucket, this thread's rows
 #pragma unroll
         for (int b = 0; b < 32; ++b) ts_acc[b] = 0.f;
@@ -234,18 +236,17 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const int n = key_tiles_count(kt);
             const int qp = q0 + r;
             const bool qok = qp < L;
-            const ChunkCtx cx{a.pos ? pos_s : nullptr, a.P, a.ts ? ts_s : nullptr, a.NB, a.t ? a.t + o : nullptr,
-                              a.K1, a.K2, L, a.alpha};
-            const int64_t tq = (a.ts && qok) ? __ldg(a.t + o + qp) : 0;
+            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
             int cur_b = -1;            // d time_bias run-length state (buckets are monotone along the row)
             float cur_acc = 0.f;
-            int64_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
+            int32_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
             for (int j = 0; j < n; ++j) {
                 const int k0 = key_tile_at(kt, j) * BN;
                 const int kb = k0 + wg * 32;
-                const int64_t tcur = tnext;
+                const int32_t tcur = tnext;
                 if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
-                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
+                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -258,79 +259,91 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
                 ++sc;
                 // ds' = dP (1 + t)(1 + h (1 - t)),  h = x/2, t = tanh(h)  ==  2 N ds
-                float ds[32];
-                bool oth[32];
+                // ds' = dP (1 + t)(1 + h (1 - t)),  h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
+                float hx[32];
                 int bk[32];
-                q_bias<true>(cx, ch, qp, tq, kb, sv, ds, oth, bk);
-                float tsum = 0.f;
+                q_h<true>(cx, ch, tq, sv, hx, bk);
+                uint32_t d2[16];
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float hx = 0.5f * ds[c];
-                    const float th = tanh_approx(hx);
-                    ds[c] = dp[c] * (1.0f + th) * fmaf(hx, 1.0f - th, 1.0f);
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
+                    const uint32_t t2 = tanh_bf16x2(h2);
+                    const uint32_t a1 = add_bf16x2(t2, kBf16One2);
+                    const uint32_t w = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
+                    d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, w));
                 }
-                if (ch.m) {
+                if (ch.flags & FLAG_M) {
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
-                        if (!q_visible(cx, qp, qok, kb + c)) ds[c] = 0.f;
+                        if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2, c);
                 }
                 if (!qok) {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) ds[c] = 0.f;
+                    for (int i = 0; i < 16; ++i) d2[i] = 0u;
                 }
+                // ---- d rab partials (fp32 accumulation of the bf16 ds')
+                if (a.dpos || a.dts) {
+                    const float tsum = sum_packed16(d2);
+                    if (a.dts && qok) {
+                        auto run_add = [&](int bb, float v) {
+                            if (bb != cur_b) {
+                                if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
+                                cur_b = bb; cur_acc = 0.f;
+                            }
+                            cur_acc += v;
+                        };
+                        if (ch.b_other == ch.b_base) {
+                            run_add(ch.b_base, tsum);
+                        } else if (ch.b_other == ch.b_base + 1) {
+                            uint32_t m2[16];
 #pragma unroll
-                for (int c = 0; c < 32; ++c) tsum += ds[c];
-                // d time_bias: run-length over buckets (non-increasing along the row)
-                if (a.dts && qok) {
-                    auto run_add = [&](int bb, float v) {
-                        if (bb != cur_b) {
-                            if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
-                            cur_b = bb; cur_acc = 0.f;
+                            for (int i = 0; i < 16; ++i)
+                                m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
+                            const float so = sum_packed16(m2);
+                            run_add(ch.b_other, so);
+                            run_add(ch.b_base, tsum - so);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) {
+                                const float2 u = unpack_bf16x2(d2[c >> 1]);
+                                run_add(bk[c], (c & 1) ? u.y : u.x);
+                            }
                         }
-                        cur_acc += v;
-                    };
-                    if (ch.tmode == 0) {
-                        run_add(ch.b_base, tsum);
-                    } else if (ch.tmode == 1) {
-                        float so = 0.f;
+                    }
+                    far_acc += tsum;
+                    // d pos_bias near diagonals (delta <= P-2): delta = C + lane - c with C a multiple of 32;
+                    // a skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
+                    if (a.dpos) {
+                        const int C = q0 - k0 + 32 * (wq - wg);
+                        if (C >= -31 && C <= a.P + 29) {   // warp-uniform
+                            float lo_s = 0.f, hi_s = 0.f;
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) so += oth[c] ? ds[c] : 0.f;
-                        run_add(ch.b_other, so);
-                        run_add(ch.b_base, tsum - so);
-                    } else {
+                            for (int c = 0; c < 32; ++c) {
+                                const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (lane + c) & 31));
+                                const float xv = (c & 1) ? u.y : u.x;
+                                if (lane + c < 32) lo_s += xv; else hi_s += xv;
+                            }
+                            const int dlo = C + lane, dhi = C + lane - 32;
+                            const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
+                            const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) run_add(bk[c], ds[c]);
+                            for (int t = 0; t < kMaxNearT; ++t) {
+                                dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
+                                dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
+                            }
+                            far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
+                        }
                     }
                 }
-                far_acc += tsum;
                 // ---- dS' (bf16) -> smem for dQ += dS K
                 const int db = dc & 1;
                 mbar_wait(&bars->ds_empty[db], ((dc >> 1) & 1) ^ 1);
                 uint8_t* tile = sdS + db * ST;
-                store_bf16_row32(tile, r, wg * 32, ds);
+                store_row32_packed(tile, r, wg * 32, d2);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_full[db]);
                 ++dc;
-                // ---- d pos_bias near diagonals (delta <= P-2) from the bf16 dS' tile
-                if (a.dpos) {
-                    const int D0 = q0 - k0;
-                    const int lo = imax(0, D0 - (BN - 1)), hi = imin(a.P - 2, D0 + BM - 1);
-                    if (lo <= hi) {
-                        named_bar_sync(1, 256);
-                        // one owner thread per diagonal: no atomics, smem accumulator per CTA
-                        const int nd = hi - lo + 1;
-                        for (int idx = et; idx < nd; idx += 256) {
-                            const int delta = lo + idx;
-                            float sum = 0.f;
-                            const int i0 = imax(0, delta - D0), i1 = imin(BM, delta - D0 + BN);
-                            for (int i = i0; i < i1; ++i) sum += load_bf16_sw(tile, i, i + D0 - delta);
-                            dpos_s[delta] += sum;
-                            far_acc -= sum;
-                        }
-                        named_bar_sync(1, 256);
-                    }
-                }
             }
             // ---- close this item's time-bucket run
             if (a.dts && cur_b >= 0) ts_acc[cur_b] += cur_acc;
@@ -354,10 +367,16 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #pragma unroll
                 for (int b = 0; b < 32; ++b) red[b * 256 + et] = ts_acc[b];
             }
+            float* redp = red + 32 * 256;                        // [kMaxNearT*32][8 warps]
+            const int ew = et >> 5;
+            if (a.dpos) {
+#pragma unroll
+                for (int t = 0; t < kMaxNearT; ++t) redp[(t * 32 + lane) * 8 + ew] = dpr[t];
+            }
             float f = far_acc;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
-            if (lane == 0) red[32 * 256 + (et >> 5)] = f;
+            if (lane == 0) redp[kMaxNearT * 32 * 8 + ew] = f;
             named_bar_sync(2, 256);
             if (a.dts && et < a.NB) {
                 float sum = 0.f;
@@ -365,14 +384,18 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 if (sum != 0.f) atomicAdd(a.dts + et, sum * rscale);
             }
             if (a.dpos) {
+                if (et < a.P - 1) {
+                    float sum = 0.f;
+#pragma unroll
+                    for (int w8 = 0; w8 < 8; ++w8) sum += redp[et * 8 + w8];
+                    if (sum != 0.f) atomicAdd(a.dpos + et, sum * rscale);
+                }
                 if (et == 0) {
                     float sum = 0.f;
-                    for (int i = 0; i < 8; ++i) sum += red[32 * 256 + i];
-                    dpos_s[a.P - 1] += sum;
+#pragma unroll
+                    for (int w8 = 0; w8 < 8; ++w8) sum += redp[kMaxNearT * 32 * 8 + w8];
+                    if (sum != 0.f) atomicAdd(a.dpos + a.P - 1, sum * rscale);
                 }
-                named_bar_sync(2, 256);
-                for (int i = et; i < a.P; i += 256)
-                    if (dpos_s[i] != 0.f) atomicAdd(a.dpos + i, dpos_s[i] * rscale);
             }
         }
     }
@@ -388,7 +411,7 @@ constexpr int KT = 128 * 128 * 2;         // K / V tile bytes
 constexpr int QT = 64 * 128 * 2;          // Q / dA tile bytes
 constexpr int PT = 128 * 64 * 2;          // P^T / dS^T tile bytes
 constexpr int QA_STAGES = 3;
-constexpr int SMEM = 2 * KT + QA_STAGES * 2 * QT + 2 * PT + kMaxPosSmem * 4 + 256 + 1024 + 512;
+constexpr int SMEM = 2 * KT + QA_STAGES * 2 * QT + 2 * PT + kPosTab * 4 + 256 + 1024 + 512;
 
 struct __align__(8) Bars {
     uint64_t kv_full, kv_empty;
@@ -417,7 +440,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     uint8_t* sP = sdA + QA_STAGES * QT;
     uint8_t* sdS = sP + PT;
     float* pos_s = reinterpret_cast<float*>(sdS + PT);
-    float* ts_s = pos_s + kMaxPosSmem;
+    float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -534,15 +557,14 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const int n = n_qtiles(k0, L, a.K1, a.K2);
             const int kp = k0 + r;
             const bool kok = kp < L;
-            const ChunkCtx cx{a.pos ? pos_s : nullptr, a.P, a.ts ? ts_s : nullptr, a.NB, a.t ? a.t + o : nullptr,
-                              a.K1, a.K2, L, a.alpha};
-            const int64_t tk = (a.ts && kok) ? __ldg(a.t + o + kp) : 0;
-            int64_t tnext = col_time(cx, (k0 / BN) * BN + wg * 32, lane);
+            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
+            int32_t tnext = col_time(cx, (k0 / BN) * BN + wg * 32, lane);
             for (int i = 0; i < n; ++i) {
                 const int qb = (k0 / BN + i) * BN + wg * 32;
-                const int64_t tcur = tnext;
+                const int32_t tcur = tnext;
                 if (i + 1 < n) tnext = col_time(cx, (k0 / BN + i + 1) * BN + wg * 32, lane);
-                const Chunk ch = k_chunk(cx, kp, kok, tk, qb, lane, tcur);
+                const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
                 const int sb = sc & 1;
                 mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
@@ -555,24 +577,27 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
                 ++sc;
                 // p' = silu(x) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  h = x/2, t = tanh(h)
-                float p[32], ds[32];
-                k_bias(cx, ch, kp, tk, qb, sv, p);
+                // p' = silu(2h) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  t = tanh(h); bf16x2
+                float hx[32];
+                k_h(cx, ch, tk, sv, hx);
+                uint32_t p2[16], d2[16];
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float hx = 0.5f * p[c];
-                    const float th = tanh_approx(hx);
-                    const float a1 = 1.0f + th;
-                    p[c] = hx * a1;
-                    ds[c] = dp[c] * a1 * fmaf(hx, 1.0f - th, 1.0f);
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
+                    const uint32_t t2 = tanh_bf16x2(h2);
+                    const uint32_t a1 = add_bf16x2(t2, kBf16One2);
+                    p2[i] = mul_bf16x2(h2, a1);
+                    const uint32_t w = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
+                    d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, w));
                 }
-                if (ch.m) {
+                if (ch.flags & FLAG_M) {
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
-                        if (!k_visible(cx, kp, kok, qb + c)) { p[c] = 0.f; ds[c] = 0.f; }
+                        if (!k_visible(cx, kp, kok, qb + c)) { zero_half(p2, c); zero_half(d2, c); }
                 }
                 mbar_wait(&bars->p_empty, (pc & 1) ^ 1);
-                store_bf16_row32(sP, r, wg * 32, p);
-                store_bf16_row32(sdS, r, wg * 32, ds);
+                store_row32_packed(sP, r, wg * 32, p2);
+                store_row32_packed(sdS, r, wg * 32, d2);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full);

@@ -87,178 +87,205 @@ UH_HD int query_end(int k0, int rows, int L, int K1, int K2) {
 // The epilogue budget is ~8 lane-ops per score element at full tensor rate, so
 // the mask and the rab bias are resolved per 32-column chunk and every
 // per-element component is switched on only when some lane of the warp needs it
-// (warp-uniform flags, so no divergence):
-//   m     per-element mask (the chunk crosses the diagonal, the band edge, or L)
-//   pp    per-element position bias (the chunk is within P-1 of the diagonal)
-//   tmode 0: the time bucket is constant along every lane's chunk
-//         1: at most two buckets per lane -> one threshold compare per element
-//         2: generic per-element bucket (only right next to the diagonal)
-// Buckets of floor(log2 dt) are monotone along a row because timestamps are
-// sorted, so a lane's chunk has buckets b_first..b_last and "two buckets" means
-// one threshold on the column timestamp.  rab tables live in smem (pos_s: P
-// floats, ts_s: NB <= 32 floats).  Rows beyond L are "don't care" (their outputs
-// are never stored) and never force a per-element component.
-// Column timestamps are carried per lane as 32-bit offsets from the chunk's
-// first column (chunks must span < 2^31 s).
+// (warp-uniform flags from one redux.or, so no divergence):
+//   FLAG_M   per-element mask (the chunk crosses the diagonal, the band edge, or L)
+//   FLAG_P   per-element position bias (the chunk is within P-1 of the diagonal):
+//            one LDS with an immediate offset from an extended table
+//   FLAG_T1  some lane sees two time buckets: the columns of the larger-dt bucket
+//            form a prefix (queries as rows) / suffix (keys as rows) whose length a
+//            5-step binary search over the lanes' column timestamps finds
+//   FLAG_T2  some lane sees >2 buckets (right next to the diagonal): per element
+// Buckets floor(log2 dt) are monotone along a row because timestamps are sorted.
+// Everything carries h = x/2 (x = alpha S + rab), the argument of tanh in
+// silu(x) = h + h tanh(h); tables are pre-halved.  Timestamps are 32-bit offsets
+// from the sequence's first timestamp (a sequence must span < 2^31 s).
+// Rows beyond L are "don't care" (never stored) and never raise a flag.
 // ----------------------------------------------------------------------------
+constexpr int kPosPad = 64;        // extended position table covers dd in [-64, P+31]
+constexpr int kMaxPosSmem = 256;   // bf16 tcgen05 path: pos_bias_len <= 256 (validated)
+constexpr int kMaxNearT = kMaxPosSmem / 32;  // near-diagonal register partials per lane (dQ kernel)
+constexpr int kPosTab = kMaxPosSmem + 96;
+enum { FLAG_M = 1, FLAG_P = 2, FLAG_T1 = 4, FLAG_T2 = 8 };
+
 struct ChunkCtx {
-    const float* pos_s; int P;
-    const float* ts_s; int NB;
-    const int64_t* t;   // timestamps of this sequence (t + seq_start) or nullptr
+    const float* pos_e;  // smem: pos_e[dd + kPosPad] = (pos[clamp(dd)] - pos[P-1]) / 2, or nullptr
+    float pos_far;       // pos[P-1] / 2
+    int P;
+    const float* ts_h;   // smem: ts / 2, or nullptr
+    int NB;
+    const int64_t* t;    // timestamps of this sequence (t + seq_start)
+    int64_t t0;          // first timestamp of the sequence (32-bit offsets are relative to it)
     int K1, K2, L;
-    float alpha;
+    float ha;            // alpha / 2
 };
 
-UH_DEV int64_t shfl64(int64_t v, int src) {
-    int lo = __shfl_sync(0xffffffffu, (int)(v & 0xffffffff), src);
-    int hi = __shfl_sync(0xffffffffu, (int)(v >> 32), src);
-    return ((int64_t)hi << 32) | (uint32_t)lo;
+UH_DEV int32_t rel32(int64_t t, int64_t t0) {
+    int64_t d = t - t0;
+    return (int32_t)(d < 0 ? 0 : (d > 0x7fffffffLL ? 0x7fffffffLL : d));
 }
-
-UH_DEV int32_t clamp_i32(int64_t v) {
-    return (int32_t)(v < -1 ? -1 : (v > 0x7fffffffLL ? 0x7fffffffLL : v));
+UH_DEV int bucket32(int32_t dt, int NB) {  // min(NB-1, floor(log2(max(dt,1))))
+    const int b = 31 - __clz(dt < 1 ? 1 : dt);
+    return b < NB - 1 ? b : NB - 1;
 }
-
-// tcol: this lane's column timestamp t[col0 + lane] (prefetched one tile ahead by the caller)
-UH_DEV int64_t col_time(const ChunkCtx& c, int col0, int lane) {
-    return c.ts_s ? __ldg(c.t + imin(col0 + lane, c.L - 1)) : 0;
+// column timestamp of this lane for the chunk starting at col0 (prefetched a tile ahead)
+UH_DEV int32_t col_time(const ChunkCtx& c, int col0, int lane) {
+    return c.ts_h ? rel32(__ldg(c.t + imin(col0 + lane, c.L - 1)), c.t0) : 0;
 }
 
 struct Chunk {
-    bool m, pp;       // warp-uniform: per-element mask / position bias needed
-    int tmode;        // warp-uniform: 0 constant bucket, 1 threshold, 2 generic
-    float bias;       // per lane: constant part of the bias (pos[P-1] and ts[b_base])
-    float tdelta;     // per lane (tmode 1): ts[b_other] - ts[b_base]
-    int32_t thr;      // per lane (tmode 1): column offset threshold of the b_other side
-    int32_t rel;      // per lane: this lane's column timestamp - chunk base
+    unsigned flags;   // warp-uniform OR of FLAG_*
+    float hbias;      // per lane: constant part of h's bias (pos_far + ts_h[b_base])
+    float hbias_o;    // per lane: bias of the "other" time bucket (FLAG_T1)
+    int n;            // per lane (FLAG_T1): q-rows: columns [0,n) are in the other bucket;
+                      //                      k-rows: columns [n,32) are in the other bucket
     int b_base, b_other;
-    int64_t tcol;     // per lane: column timestamp (tmode 2)
+    int bd;           // per lane: clamped qp-kb (q-rows) / qb-kp (k-rows) for the position table
+    int32_t tcol;     // per lane: column timestamp (32-bit offset)
 };
 
+// number of lanes c whose value v[c] (non-decreasing in c) satisfies v[c] <= x (less=false) or v[c] < x (less=true)
+template <bool LESS>
+UH_DEV int count_le(int32_t v, int32_t x) {
+    int lo = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+        const int32_t w = __shfl_sync(0xffffffffu, v, lo + step - 1);
+        if (LESS ? (w < x) : (w <= x)) lo += step;
+    }
+    // lo in [0, 31]; include lane 31 if it also satisfies
+    const int32_t w = __shfl_sync(0xffffffffu, v, 31);
+    if (lo == 31 && (LESS ? (w < x) : (w <= x))) lo = 32;
+    return lo;
+}
+
 // rows are queries (forward, dQ); columns are keys kb..kb+31 (dt decreasing along the row)
-UH_DEV Chunk q_chunk(const ChunkCtx& c, int qp, bool qok, int64_t tq, int kb, int lane, int64_t tcol) {
+UH_DEV Chunk q_chunk(const ChunkCtx& c, int qp, bool qok, int32_t tq, int kb, int32_t tcol) {
     Chunk r;
-    const bool full = (kb + 31 <= qp) && (qp - kb <= c.K1 || kb + 31 < c.K2);
-    bool pp = false;
-    float bias = 0.f;
-    if (c.pos_s) {
-        pp = qp - kb - 31 < c.P - 1;
-        bias += c.pos_s[c.P - 1];
+    unsigned f = 0;
+    if (!((kb + 31 <= qp) && (qp - kb <= c.K1 || kb + 31 < c.K2))) f |= FLAG_M;
+    float hb = 0.f;
+    r.bd = 0;
+    if (c.pos_e) {
+        const int d0 = qp - kb;
+        if (d0 - 31 < c.P - 1) f |= FLAG_P;
+        r.bd = d0 < -32 ? -32 : (d0 > c.P + 31 ? c.P + 31 : d0);
+        hb += c.pos_far;
     }
-    int tm = 0;
-    r.tdelta = 0.f; r.thr = -1; r.rel = 0; r.b_base = 0; r.b_other = 0; r.tcol = tcol;
-    if (c.ts_s) {
-        const int64_t base = shfl64(tcol, 0);
-        const int bf = time_bucket(tq - base, c.NB);                 // first column: largest dt
-        const int bl = time_bucket(tq - shfl64(tcol, 31), c.NB);     // last column: smallest dt
+    r.tcol = tcol;
+    r.b_base = r.b_other = 0;
+    r.hbias_o = 0.f;
+    r.n = 0;
+    int32_t thr = 0;
+    if (c.ts_h) {
+        const int bf = bucket32(tq - __shfl_sync(0xffffffffu, tcol, 0), c.NB);   // first column: largest dt
+        const int bl = bucket32(tq - __shfl_sync(0xffffffffu, tcol, 31), c.NB);  // last column: smallest dt
         r.b_base = bl; r.b_other = bf;
-        r.rel = clamp_i32(tcol - base);
-        tm = bf == bl ? 0 : (bf == bl + 1 ? 1 : 2);
-        if (tm == 1) {
-            r.tdelta = c.ts_s[bf] - c.ts_s[bl];
-            r.thr = clamp_i32(tq - (int64_t(1) << bf) - base);     // column in b_other iff rel <= thr
-        }
-        bias += c.ts_s[bl];
+        if (bf == bl + 1) f |= FLAG_T1;
+        else if (bf > bl + 1) f |= FLAG_T2;
+        const int64_t th = (int64_t)tq - ((int64_t)1 << bf);                   // other bucket iff tcol <= th
+        thr = (int32_t)(th < -1 ? -1 : th);
+        r.hbias_o = hb + c.ts_h[bf];
+        hb += c.ts_h[bl];
     }
-    r.m = __any_sync(0xffffffffu, qok && !full);
-    r.pp = __any_sync(0xffffffffu, qok && pp);
-    const int t1 = __any_sync(0xffffffffu, qok && tm >= 1), t2 = __any_sync(0xffffffffu, qok && tm == 2);
-    r.tmode = t2 ? 2 : (t1 ? 1 : 0);
-    r.bias = bias;
+    r.flags = __reduce_or_sync(0xffffffffu, qok ? f : 0u);
+    if (r.flags & FLAG_T1) {
+        const int cnt = count_le<false>(tcol, thr);   // all lanes take part in the shuffles
+        r.n = (r.b_other == r.b_base + 1) ? cnt : 0;
+    }
+    r.hbias = hb;
     return r;
 }
 
 // rows are keys (dK/dV); columns are queries qb..qb+31 (dt increasing along the row)
-UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int64_t tk, int qb, int lane, int64_t tcol) {
+UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int32_t tk, int qb, int32_t tcol) {
     Chunk r;
-    const bool full = (qb >= kp) && (qb + 31 < c.L) && (qb + 31 - kp <= c.K1 || kp < c.K2);
-    bool pp = false;
-    float bias = 0.f;
-    if (c.pos_s) {
-        pp = qb - kp < c.P - 1;
-        bias += c.pos_s[c.P - 1];
+    unsigned f = 0;
+    if (!((qb >= kp) && (qb + 31 < c.L) && (qb + 31 - kp <= c.K1 || kp < c.K2))) f |= FLAG_M;
+    float hb = 0.f;
+    r.bd = 0;
+    if (c.pos_e) {
+        const int d0 = qb - kp;
+        if (d0 < c.P - 1) f |= FLAG_P;
+        r.bd = d0 < -64 ? -64 : (d0 > c.P ? c.P : d0);
+        hb += c.pos_far;
     }
-    int tm = 0;
-    r.tdelta = 0.f; r.thr = 0x7fffffff; r.rel = 0; r.b_base = 0; r.b_other = 0; r.tcol = tcol;
-    if (c.ts_s) {
-        const int64_t base = shfl64(tcol, 0);
-        const int bf = time_bucket(base - tk, c.NB);                 // first column: smallest dt
-        const int bl = time_bucket(shfl64(tcol, 31) - tk, c.NB);     // last column: largest dt
+    r.tcol = tcol;
+    r.b_base = r.b_other = 0;
+    r.hbias_o = 0.f;
+    r.n = 32;
+    int32_t thr = 0;
+    if (c.ts_h) {
+        const int bf = bucket32(__shfl_sync(0xffffffffu, tcol, 0) - tk, c.NB);   // first column: smallest dt
+        const int bl = bucket32(__shfl_sync(0xffffffffu, tcol, 31) - tk, c.NB);  // last column: largest dt
         r.b_base = bf; r.b_other = bl;
-        r.rel = clamp_i32(tcol - base);
-        tm = bf == bl ? 0 : (bl == bf + 1 ? 1 : 2);
-        if (tm == 1) {
-            r.tdelta = c.ts_s[bl] - c.ts_s[bf];
-            r.thr = clamp_i32(tk + (int64_t(1) << bl) - base);     // column in b_other iff rel >= thr
-        }
-        bias += c.ts_s[bf];
+        if (bl == bf + 1) f |= FLAG_T1;
+        else if (bl > bf + 1) f |= FLAG_T2;
+        const int64_t th = (int64_t)tk + ((int64_t)1 << bl);                   // other bucket iff tcol >= th
+        thr = (int32_t)(th > 0x7fffffffLL ? 0x7fffffffLL : th);
+        r.hbias_o = hb + c.ts_h[bl];
+        hb += c.ts_h[bf];
     }
-    r.m = __any_sync(0xffffffffu, kok && !full);
-    r.pp = __any_sync(0xffffffffu, kok && pp);
-    const int t1 = __any_sync(0xffffffffu, kok && tm >= 1), t2 = __any_sync(0xffffffffu, kok && tm == 2);
-    r.tmode = t2 ? 2 : (t1 ? 1 : 0);
-    r.bias = bias;
+    r.flags = __reduce_or_sync(0xffffffffu, kok ? f : 0u);
+    if (r.flags & FLAG_T1) {
+        const int cnt = count_le<true>(tcol, thr);    // all lanes take part in the shuffles
+        r.n = (r.b_other == r.b_base + 1) ? cnt : 32;
+    }
+    r.hbias = hb;
     return r;
 }
 
-// x[c] = alpha * s[c] + rab(c) for a query-row chunk; returns the per-element bucket
-// in bk[] only when tmode == 2 (else bk is untouched).  Masking is separate (q_mask).
+// h[j] = (alpha S + rab)/2 for a query-row chunk.  With WANT_BUCKET the per-element
+// time bucket is returned in bk[] when FLAG_T2 is set.
 template <bool WANT_BUCKET>
-UH_DEV void q_bias(const ChunkCtx& c, const Chunk& ch, int qp, int64_t tq, int kb, const float* s, float* x,
-                   bool* other, int* bk) {
+UH_DEV void q_h(const ChunkCtx& c, const Chunk& ch, int32_t tq, const float* s, float* h, int* bk) {
+    if (ch.flags & FLAG_T1) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = fmaf(s[j], c.alpha, ch.bias);
-    if (ch.pp) {
-        const float pl = c.pos_s[c.P - 1];
+        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, j < ch.n ? ch.hbias_o : ch.hbias);
+    } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            int dd = qp - kb - j;
-            dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1);
-            x[j] += c.pos_s[dd] - pl;
-        }
+        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, ch.hbias);
     }
-    if (ch.tmode == 1) {
+    if (ch.flags & FLAG_P) {
+        const float* pe = c.pos_e + kPosPad + ch.bd;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h[j] += pe[-j];
+    }
+    if (ch.flags & FLAG_T2) {
+        const float tb = c.ts_h[ch.b_base];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            const bool o = __shfl_sync(0xffffffffu, ch.rel, j) <= ch.thr;
-            if (WANT_BUCKET) other[j] = o;
-            x[j] += o ? ch.tdelta : 0.f;
-        }
-    } else if (ch.tmode == 2) {
-        const float tb = c.ts_s[ch.b_base];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int b = time_bucket(tq - shfl64(ch.tcol, j), c.NB);
+            const int b = bucket32(tq - __shfl_sync(0xffffffffu, ch.tcol, j), c.NB);
             if (WANT_BUCKET) bk[j] = b;
-            x[j] += c.ts_s[b] - tb;
+            h[j] += (ch.b_other == ch.b_base + 1 || ch.b_other == ch.b_base) ? 0.f : c.ts_h[b] - tb;
         }
     }
 }
 
 // the same for a key-row chunk (columns are queries)
-UH_DEV void k_bias(const ChunkCtx& c, const Chunk& ch, int kp, int64_t tk, int qb, const float* s, float* x) {
+UH_DEV void k_h(const ChunkCtx& c, const Chunk& ch, int32_t tk, const float* s, float* h) {
+    if (ch.flags & FLAG_T1) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) x[j] = fmaf(s[j], c.alpha, ch.bias);
-    if (ch.pp) {
-        const float pl = c.pos_s[c.P - 1];
+        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, j >= ch.n ? ch.hbias_o : ch.hbias);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, ch.hbias);
+    }
+    if (ch.flags & FLAG_P) {
+        const float* pe = c.pos_e + kPosPad + ch.bd;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h[j] += pe[j];
+    }
+    if (ch.flags & FLAG_T2) {
+        const float tb = c.ts_h[ch.b_base];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            int dd = qb + j - kp;
-            dd = dd < 0 ? 0 : (dd < c.P - 1 ? dd : c.P - 1);
-            x[j] += c.pos_s[dd] - pl;
+            const int b = bucket32(__shfl_sync(0xffffffffu, ch.tcol, j) - tk, c.NB);
+            h[j] += (ch.b_other == ch.b_base + 1 || ch.b_other == ch.b_base) ? 0.f : c.ts_h[b] - tb;
         }
-    }
-    if (ch.tmode == 1) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] += (__shfl_sync(0xffffffffu, ch.rel, j) >= ch.thr) ? ch.tdelta : 0.f;
-    } else if (ch.tmode == 2) {
-        const float tb = c.ts_s[ch.b_base];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] += c.ts_s[time_bucket(shfl64(ch.tcol, j) - tk, c.NB)] - tb;
     }
 }
 
-// per-element visibility (only called when ch.m)
+// per-element visibility (only needed when FLAG_M)
 UH_DEV bool q_visible(const ChunkCtx& c, int qp, bool qok, int kp) {
     return qok && kp < c.L && mask_ok(qp, kp, c.K1, c.K2);
 }
@@ -266,15 +293,56 @@ UH_DEV bool k_visible(const ChunkCtx& c, int kp, bool kok, int qp) {
     return kok && qp < c.L && mask_ok(qp, kp, c.K1, c.K2);
 }
 
-
-// Stage the rab tables into shared memory (all threads of the CTA; caller syncs).
-UH_DEV void stage_rab(const AttnArgs& a, float* pos_s, float* ts_s) {
-    if (a.pos)
-        for (int i = threadIdx.x; i < a.P; i += blockDim.x) pos_s[i] = __ldg(a.pos + i);
-    if (a.ts)
-        for (int i = threadIdx.x; i < a.NB; i += blockDim.x) ts_s[i] = __ldg(a.ts + i);
+// row r of a [rows x 64] bf16 K-major SW128 tile: 32 packed columns (16 x bf16x2) at col0 (0 or 32)
+UH_DEV void store_row32_packed(uint8_t* tile, int r, int col0, const uint32_t* v) {
+    uint8_t* row = tile + r * 128;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int ch = (col0 >> 3) + c;
+        *reinterpret_cast<uint4*>(row + ((ch ^ (r & 7)) << 4)) =
+            make_uint4(v[4 * c + 0], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
+}
+// zero element j (low half for even j, high half for odd j) of a packed bf16x2 array
+UH_DEV void zero_half(uint32_t* v, int j) { v[j >> 1] &= (j & 1) ? 0x0000FFFFu : 0xFFFF0000u; }
+// sum of 16 packed bf16x2 values, pairwise in bf16x2, final pair in fp32
+UH_DEV float sum_packed16(const uint32_t* v) {
+    uint32_t a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = add_bf16x2(v[i], v[i + 8]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = add_bf16x2(a[i], a[i + 4]);
+    a[0] = add_bf16x2(a[0], a[2]); a[1] = add_bf16x2(a[1], a[3]);
+    const float2 x = unpack_bf16x2(a[0]), y = unpack_bf16x2(a[1]);
+    return (x.x + x.y) + (y.x + y.y);
 }
 
-constexpr int kMaxPosSmem = 2048;  // bf16 tcgen05 path: pos_bias_len <= 2048 (validated)
+// Stage the pre-halved rab tables into shared memory (all threads; caller syncs).
+UH_DEV void stage_rab(const AttnArgs& a, float* pos_e, float* ts_h) {
+    if (a.pos) {
+        const float far = __ldg(a.pos + a.P - 1);
+        for (int i = threadIdx.x; i < a.P + 96; i += blockDim.x) {
+            int dd = i - kPosPad;
+            dd = dd < 0 ? 0 : (dd > a.P - 1 ? a.P - 1 : dd);
+            pos_e[i] = 0.5f * (__ldg(a.pos + dd) - far);
+        }
+    }
+    if (a.ts)
+        for (int i = threadIdx.x; i < a.NB; i += blockDim.x) ts_h[i] = 0.5f * __ldg(a.ts + i);
+}
+
+UH_DEV ChunkCtx make_ctx(const AttnArgs& a, const float* pos_e, const float* ts_h, int o, int L) {
+    ChunkCtx c;
+    c.pos_e = a.pos ? pos_e : nullptr;
+    c.pos_far = a.pos ? 0.5f * __ldg(a.pos + a.P - 1) : 0.f;
+    c.P = a.P;
+    c.ts_h = a.ts ? ts_h : nullptr;
+    c.NB = a.NB;
+    c.t = a.t ? a.t + o : nullptr;
+    c.t0 = a.ts ? __ldg(a.t + o) : 0;
+    c.K1 = a.K1; c.K2 = a.K2; c.L = L;
+    c.ha = 0.5f * a.alpha;
+    return c;
+}
 
 }  // namespace uh

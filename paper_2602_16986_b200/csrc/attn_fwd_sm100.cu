@@ -31,15 +31,19 @@ constexpr int BM = 128, BN = 64, DH = 128;
 constexpr int QT = BM * DH * 2;          // 32 KB: Q tile, two 64-column swizzled blocks of 16 KB
 constexpr int KT = BN * DH * 2;          // 16 KB: K (or V) tile, two 8 KB blocks
 constexpr int PT = BM * BN * 2;          // 16 KB: P tile, one block
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;               // (K,V) smem ring
+constexpr int NS = 3;                   // S buffers in TMEM (64 columns each)
+constexpr int LAG = NS - 1;             // the MMA issues S(j) LAG tiles ahead of PV(j)
+constexpr int O_COL = 256;              // TMEM column of the O accumulator
+constexpr int Q_COL = 384;              // TMEM columns of Q (A operand of S = Q K^T), 64 packed columns
 constexpr int NUM_THREADS = 384;
-constexpr int SMEM_BYTES = QT + STAGES * 2 * KT + 2 * PT + kMaxPosSmem * 4 + 256 + 1024 + 512;
+constexpr int SMEM_BYTES = QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512;
 
 struct __align__(8) FwdBars {
     uint64_t q_full, q_empty;
     uint64_t kv_full[STAGES], kv_empty[STAGES];
-    uint64_t s_full[2], s_empty[2];
-    uint64_t p_full[2], p_empty[2];
+    uint64_t s_full[NS];
+    uint64_t p_full[NS];
     uint64_t o_full, o_empty;
     uint32_t tmem;
 };
@@ -62,9 +66,8 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
     uint8_t* sKV = smem + QT;                     // [STAGES] x (K 16K | V 16K)
-    uint8_t* sP = sKV + STAGES * 2 * KT;          // [2]
-    float* pos_s = reinterpret_cast<float*>(sP + 2 * PT);
-    float* ts_s = pos_s + kMaxPosSmem;
+    float* pos_s = reinterpret_cast<float*>(sKV + STAGES * 2 * KT);
+    float* ts_s = pos_s + kPosTab;
     FwdBars* bars = reinterpret_cast<FwdBars*>(ts_s + 64);
 
     const int warp = threadIdx.x >> 5;
@@ -73,16 +76,13 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     if (threadIdx.x == 0) {
         mbar_init(&bars->q_full, 1); mbar_init(&bars->q_empty, 1);
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bars->s_full[i], 1); mbar_init(&bars->s_empty[i], 8);
-            mbar_init(&bars->p_full[i], 8); mbar_init(&bars->p_empty[i], 1);
-        }
+        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 8); }
         mbar_init(&bars->o_full, 1); mbar_init(&bars->o_empty, 8);
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
     if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmQ); tma_prefetch_desc(&tmK); tma_prefetch_desc(&tmV); }
-    if (warp == 2) tmem_alloc<256>(&bars->tmem);
+    if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -121,57 +121,60 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         constexpr uint32_t idesc_o = make_idesc_bf16(BM, DH, false, true);   // P (K-major) x V (MN-major)
         int kc = 0, sc = 0, pc = 0, qi = 0;
         const uint32_t q_addr = smem_u32(sQ);
-        auto issue_pv = [&](int jj, int stage) {
-            const int pb = pc & 1;
-            mbar_wait(&bars->p_full[pb], (pc >> 1) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t p_addr = smem_u32(sP + pb * PT);
-                const uint32_t v_addr = smem_u32(sKV + stage * 2 * KT + KT);
-#pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk)
-                    umma_ss(tmem + 128, make_sw128_desc(p_addr + kk * 32, 16, 1024),
-                            make_sw128_desc(v_addr + kk * 2048, KT / 2, 1024), idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&bars->p_empty[pb]);
-                umma_commit(&bars->kv_empty[stage]);
-            }
-            __syncwarp();
-            ++pc;
-        };
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
             const WorkItem it = a.items[w];
             const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
             const int n = key_tiles_count(kt);
+            const int kc0 = kc;
             mbar_wait(&bars->q_full, qi & 1);
-            int prev = 0;
-            for (int j = 0; j < n; ++j) {
-                const int s = kc % STAGES, sb = sc & 1;
-                mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
-                mbar_wait(&bars->s_empty[sb], ((sc >> 1) & 1) ^ 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t k_addr = smem_u32(sKV + s * 2 * KT);
+            tc_fence_after();
+            if (elect_one()) {   // Q: smem -> TMEM once per item (in order with the MMAs that read it)
 #pragma unroll
-                    for (int kk = 0; kk < DH / 16; ++kk)
-                        umma_ss(tmem + sb * BN, make_sw128_desc(q_addr + (kk >> 2) * (QT / 2) + (kk & 3) * 32, 16, 1024),
-                                make_sw128_desc(k_addr + (kk >> 2) * (KT / 2) + (kk & 3) * 32, 16, 1024), idesc_s,
-                                kk > 0 ? 1u : 0u);
-                    umma_commit(&bars->s_full[sb]);
-                    if (j == n - 1) umma_commit(&bars->q_empty);
-                }
-                __syncwarp();
-                ++sc;
-                if (j >= 1) {
-                    if (j == 1) mbar_wait(&bars->o_empty, (qi & 1) ^ 1);
-                    issue_pv(j - 1, prev);
-                }
-                prev = s;
-                ++kc;
+                for (int kk = 0; kk < DH / 16; ++kk)
+                    tmem_cp_128x256b(tmem + Q_COL + kk * 8,
+                                     make_sw128_desc(q_addr + (kk >> 2) * (QT / 2) + (kk & 3) * 32, 16, 1024));
+                umma_commit(&bars->q_empty);
             }
-            if (n == 1) mbar_wait(&bars->o_empty, (qi & 1) ^ 1);
-            issue_pv(n - 1, prev);
-            if (elect_one()) umma_commit(&bars->o_full);
             __syncwarp();
+            for (int j = 0; j < n + LAG; ++j) {
+                if (j < n) {   // ---- S(j) = Q K_j^T
+                    // buffer sb was last read by PV(j - NS), issued earlier: the tensor pipe is in order
+                    const int s = kc % STAGES, sb = sc % NS;
+                    mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t k_addr = smem_u32(sKV + s * 2 * KT);
+#pragma unroll
+                        for (int kk = 0; kk < DH / 16; ++kk)
+                            umma_ts(tmem + sb * BN, tmem + Q_COL + kk * 8,
+                                    make_sw128_desc(k_addr + (kk >> 2) * (KT / 2) + (kk & 3) * 32, 16, 1024), idesc_s,
+                                    kk > 0 ? 1u : 0u);
+                        umma_commit(&bars->s_full[sb]);
+                    }
+                    __syncwarp();
+                    ++sc; ++kc;
+                }
+                if (j >= LAG) {   // ---- O += P(jj) V_jj
+                    const int jj = j - LAG;
+                    const int stage = (kc0 + jj) % STAGES, pb = pc % NS;
+                    if (jj == 0) mbar_wait(&bars->o_empty, (qi & 1) ^ 1);
+                    mbar_wait(&bars->p_full[pb], (pc / NS) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        // P(jj) lives in TMEM over the consumed S columns: keys [32g, 32g+32) at column 32g
+                        const uint32_t v_addr = smem_u32(sKV + stage * 2 * KT + KT);
+#pragma unroll
+                        for (int kk = 0; kk < BN / 16; ++kk)
+                            umma_ts(tmem + O_COL, tmem + pb * BN + (kk >> 1) * 32 + (kk & 1) * 8,
+                                    make_sw128_desc(v_addr + kk * 2048, KT / 2, 1024), idesc_o,
+                                    (jj > 0 || kk > 0) ? 1u : 0u);
+                        umma_commit(&bars->kv_empty[stage]);
+                        if (jj == n - 1) umma_commit(&bars->o_full);
+                    }
+                    __syncwarp();
+                    ++pc;
+                }
+            }
         }
     } else if (warp >= 4) {
         // ============================================================ epilogue
@@ -189,42 +192,48 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int n = key_tiles_count(kt);
             const int qp = q0 + r;
             const bool qok = qp < L;
-            const ChunkCtx cx{a.pos ? pos_s : nullptr, a.P, a.ts ? ts_s : nullptr, a.NB, a.t ? a.t + o : nullptr,
-                              a.K1, a.K2, L, a.alpha};
-            const int64_t tq = (a.ts && qok) ? __ldg(a.t + o + qp) : 0;
-            int64_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
+            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
+            int32_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
             for (int j = 0; j < n; ++j) {
                 const int kb = key_tile_at(kt, j) * BN + wg * 32;
-                const int64_t tcur = tnext;
+                const int32_t tcur = tnext;
                 if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
-                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, lane, tcur);
-                const int sb = sc & 1;
-                mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
+                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, tcur);
+                const int sb = sc % NS;
+                mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
                 float s[32];
+#if UH_EXP_SKIP_EPI
+                for (int c = 0; c < 32; ++c) s[c] = 0.f;
+#else
                 tmem_ld32(tmem + lane_base + sb * BN + wg * 32, s);
                 tmem_ld_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
+#endif
                 ++sc;
-                // x = alpha S + rab;  silu(x) = h + h tanh(h), h = x/2
-                float x[32];
-                q_bias<false>(cx, ch, qp, tq, kb, s, x, nullptr, nullptr);
+                // h = (alpha S + rab)/2 in fp32, then packed bf16x2: silu(2h) = h + h tanh(h)
+                float hx[32];
+#if UH_EXP_SKIP_EPI
+                for (int c = 0; c < 32; ++c) hx[c] = s[c];
+#else
+                q_h<false>(cx, ch, tq, s, hx, nullptr);
+#endif
+                uint32_t pk[16];
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float hx = 0.5f * x[c];
-                    s[c] = fmaf(hx, tanh_approx(hx), hx);
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
+                    pk[i] = fma_bf16x2(h2, tanh_bf16x2(h2), h2);
                 }
-                if (ch.m) {
+                if (ch.flags & FLAG_M) {
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
-                        if (!q_visible(cx, qp, qok, kb + c)) s[c] = 0.0f;
+                        if (!q_visible(cx, qp, qok, kb + c)) zero_half(pk, c);
                 }
-                const int pb = pc & 1;
-                mbar_wait(&bars->p_empty[pb], ((pc >> 1) & 1) ^ 1);
-                store_bf16_row32(sP + pb * PT, r, wg * 32, s);
-                fence_proxy_async_smem();
+                // P -> TMEM over this warpgroup's own (already read) S columns
+                const int pb = pc % NS;
+                tmem_st16(tmem + lane_base + pb * BN + wg * 32, pk);
+                tmem_st_wait();
+                tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[pb]);
                 ++pc;
@@ -233,8 +242,8 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mbar_wait(&bars->o_full, qi & 1);
             tc_fence_after();
             float ov[64];
-            tmem_ld32(tmem + lane_base + 128 + wg * 64, ov);
-            tmem_ld32(tmem + lane_base + 128 + wg * 64 + 32, ov + 32);
+            tmem_ld32(tmem + lane_base + O_COL + wg * 64, ov);
+            tmem_ld32(tmem + lane_base + O_COL + wg * 64 + 32, ov + 32);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
@@ -253,7 +262,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     }
     __syncthreads();
-    if (warp == 2) tmem_dealloc<256>(tmem);
+    if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
 }  // namespace

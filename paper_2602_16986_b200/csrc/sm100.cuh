@@ -37,15 +37,15 @@ UH_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase
-// completes (or ~1 ms passes) instead of spinning and stealing issue slots.
+// try_wait: the hardware parks the thread for a short, implementation-defined time
+// while the phase is incomplete; the loop re-polls.
 UH_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok) : "r"(addr), "r"(parity), "r"(1000000u) : "memory");
+        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
     return ok != 0;
 }
 // Blocking wait on the phase with the given parity.  A wait that never completes
@@ -54,7 +54,7 @@ UH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t n = 0;
     while (!mbar_try_wait(addr, parity)) {
-        if (++n > 20000u) __trap();
+        if (++n > 400000000u) __trap();
     }
 }
 
@@ -104,12 +104,33 @@ UH_DEV void umma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t 
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T (A from tensor memory: lanes = rows, K packed 2 x bf16 per column)
+UH_DEV void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// smem -> TMEM copy of a 128-row x 256-bit (16 bf16) K-slice: row i -> lane i, 8 columns
+UH_DEV void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 // arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete
 UH_DEV void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 UH_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+UH_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 32 lanes x 16 consecutive 32-bit columns from registers (thread t -> lane base+t)
+UH_DEV void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+          "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+}
 
 // 32 lanes x 32 consecutive fp32 columns: thread t of the warp gets lane (base+t), cols c..c+31
 UH_DEV void tmem_ld32(uint32_t taddr, float* v) {
@@ -165,6 +186,23 @@ UH_DEV float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 UH_DEV float sigmoid_f(float x) { return 1.0f / (1.0f + __expf(-x)); }
 // silu via one MUFU op: silu(x) = 0.5 x (1 + tanh(x/2))
 UH_DEV float tanh_approx(float x) { float y; asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+// ---- packed bf16x2 math (epilogues): 2 elements per instruction
+UH_DEV uint32_t tanh_bf16x2(uint32_t x) { uint32_t y; asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+UH_DEV uint32_t fma_bf16x2(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d; asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d;
+}
+UH_DEV uint32_t mul_bf16x2(uint32_t a, uint32_t b) {  // a*b + (-0)
+    uint32_t d; asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(0x80008000u)); return d;
+}
+UH_DEV uint32_t add_bf16x2(uint32_t a, uint32_t b) {  // a*1 + b
+    uint32_t d; asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(0x3F803F80u), "r"(b)); return d;
+}
+UH_DEV float2 unpack_bf16x2(uint32_t v) {
+    return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
+}
+constexpr uint32_t kBf16One2 = 0x3F803F80u;     // (1, 1)
+constexpr uint32_t kBf16NegOne2 = 0xBF80BF80u;  // (-1, -1)
 
 UH_DEV uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
