@@ -25,6 +25,12 @@
 #include "internal.h"
 
 namespace uh {
+#if UH_TRACE
+__device__ long long* g_trace = nullptr;   // [role][event] timestamps of CTA 0 (trace builds only)
+#define TRACE(slot) do { if (blockIdx.x == 0 && g_trace && (slot) < 8192) g_trace[(slot)] = clock64(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
 namespace {
 
 constexpr int BM = 128, BN = 64, DH = 128;
@@ -76,7 +82,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     if (threadIdx.x == 0) {
         mbar_init(&bars->q_full, 1); mbar_init(&bars->q_empty, 1);
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
-        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 8); }
+        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 4); }
         mbar_init(&bars->o_full, 1); mbar_init(&bars->o_empty, 8);
         fence_barrier_init();
     }
@@ -141,6 +147,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     // buffer sb was last read by PV(j - NS), issued earlier: the tensor pipe is in order
                     const int s = kc % STAGES, sb = sc % NS;
                     mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
+                    if (lane == 0) TRACE(0 * 1024 + sc);
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t k_addr = smem_u32(sKV + s * 2 * KT);
@@ -159,6 +166,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     const int stage = (kc0 + jj) % STAGES, pb = pc % NS;
                     if (jj == 0) mbar_wait(&bars->o_empty, (qi & 1) ^ 1);
                     mbar_wait(&bars->p_full[pb], (pc / NS) & 1);
+                    if (lane == 0) TRACE(1 * 1024 + pc);
                     tc_fence_after();
                     if (elect_one()) {
                         // P(jj) lives in TMEM over the consumed S columns: keys [32g, 32g+32) at column 32g
@@ -178,12 +186,12 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp >= 4) {
         // ============================================================ epilogue
-        const int wg = (warp - 4) >> 2;      // key columns [32*wg, 32*wg+32) of each 64-key tile
+        const int wg = (warp - 4) >> 2;      // warpgroup: handles the tiles of global parity wg
         const int wq = warp & 3;             // TMEM lane quarter
         const int r = wq * 32 + lane;        // row of the tile
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const float ha = 0.5f * a.alpha;
-        int sc = 0, pc = 0, qi = 0;
+        int sc = 0, qi = 0;
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
             const WorkItem it = a.items[w];
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
@@ -194,49 +202,47 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const bool qok = qp < L;
             const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
-            int32_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
-            for (int j = 0; j < n; ++j) {
-                const int kb = key_tile_at(kt, j) * BN + wg * 32;
-                const int32_t tcur = tnext;
-                if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
-                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, tcur);
+            // tiles alternate between the two warpgroups (global tile parity), so one group's
+            // MUFU-bound SiLU burst overlaps the other's TMEM traffic and bookkeeping
+            for (int j = 0; j < n; ++j, ++sc) {
+                if ((sc & 1) != wg) continue;
                 const int sb = sc % NS;
+                const int k0 = key_tile_at(kt, j) * BN;
+                const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
+                if (warp == 4 && lane == 0) TRACE(2 * 1024 + (sc & 1023));
                 mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
+                if (warp == 4 && lane == 0) TRACE(3 * 1024 + (sc & 1023));
                 tc_fence_after();
-                float s[32];
-#if UH_EXP_SKIP_EPI
-                for (int c = 0; c < 32; ++c) s[c] = 0.f;
-#else
-                tmem_ld32(tmem + lane_base + sb * BN + wg * 32, s);
-                tmem_ld_wait();
-#endif
-                ++sc;
-                // h = (alpha S + rab)/2 in fp32, then packed bf16x2: silu(2h) = h + h tanh(h)
-                float hx[32];
-#if UH_EXP_SKIP_EPI
-                for (int c = 0; c < 32; ++c) hx[c] = s[c];
-#else
-                q_h<false>(cx, ch, tq, s, hx, nullptr);
-#endif
-                uint32_t pk[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
-                    pk[i] = fma_bf16x2(h2, tanh_bf16x2(h2), h2);
-                }
-                if (ch.flags & FLAG_M) {
+                for (int hc = 0; hc < 2; ++hc) {
+                    const int kb = k0 + 32 * hc;
+                    const Chunk ch = q_chunk(cx, qp, qok, tq, kb, hc ? tc1 : tc0);
+                    float s[32];
+                    tmem_ld32(tmem + lane_base + sb * BN + 32 * hc, s);
+                    tmem_ld_wait();
+                    // h = (alpha S + rab)/2 in fp32, then packed bf16x2: silu(2h) = h + h tanh(h)
+                    float hx[32];
+                    q_h<false>(cx, ch, tq, s, hx, nullptr);
+                    uint32_t pk[16];
 #pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (!q_visible(cx, qp, qok, kb + c)) zero_half(pk, c);
+                    for (int i = 0; i < 16; ++i) {
+                        const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
+                        pk[i] = fma_bf16x2(h2, tanh_bf16x2(h2), h2);
+                    }
+                    if (ch.flags & FLAG_M) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c)
+                            if (!q_visible(cx, qp, qok, kb + c)) zero_half(pk, c);
+                    }
+                    // P -> TMEM over the chunk's own (already read) S columns: keys [32hc, 32hc+32) at col 32hc
+                    tmem_st16(tmem + lane_base + sb * BN + 32 * hc, pk);
                 }
-                // P -> TMEM over this warpgroup's own (already read) S columns
-                const int pb = pc % NS;
-                tmem_st16(tmem + lane_base + pb * BN + wg * 32, pk);
+                if (warp == 4 && lane == 0) TRACE(4 * 1024 + (sc & 1023));
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->p_full[pb]);
-                ++pc;
+                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+                if (warp == 4 && lane == 0) TRACE(5 * 1024 + (sc & 1023));
             }
             // ---- O epilogue: A = O / N
             mbar_wait(&bars->o_full, qi & 1);
@@ -284,3 +290,9 @@ uh_status attn_fwd_sm100_launch(const AttnArgs& a, cudaStream_t st, int64_t T) {
 }
 
 }  // namespace uh
+
+#if UH_TRACE
+extern "C" __attribute__((visibility("default"))) int uh_trace_set(long long* p) {
+    return (int)cudaMemcpyToSymbol(uh::g_trace, &p, sizeof(p));
+}
+#endif
