@@ -55,7 +55,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
@@ -117,25 +117,6 @@ def setup_workload(cfg_name: str, world: int, rank: int, device):
                 rank_cost=cost, owner=owner)
 
 
-def grads_bucket(prm, attn, device):
-    """One flat fp32 buffer holding every parameter gradient (the all-reduce bucket)."""
-    import torch
-    shapes = [("ln1_w", prm.ln1_w), ("ln1_b", prm.ln1_b), ("w1", prm.w1), ("b1", prm.b1), ("ln2_w", prm.ln2_w),
-              ("ln2_b", prm.ln2_b), ("w2", prm.w2), ("b2", prm.b2), ("pos_bias", attn.pos_bias),
-              ("time_bias", attn.time_bias)]
-    n = sum(t.numel() for _, t in shapes if t is not None)
-    n = (n + 3) // 4 * 4 + 4 * len(shapes)
-    flat = torch.zeros(n, dtype=torch.float32, device=device)
-    views, off = {}, 0
-    for name, t in shapes:
-        if t is None:
-            views[name] = None
-            continue
-        views[name] = flat[off:off + t.numel()].view(t.shape)
-        off += (t.numel() + 3) // 4 * 4  # keep every view 16-byte aligned
-    return flat, views
-
-
 # ----------------------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -153,15 +134,14 @@ def run_ours(args, rank, world, local_rank):
     out = torch.empty_like(x)
     dx = torch.empty_like(x)
     saved = U.alloc_saved(x)
-    flat, gviews = grads_bucket(prm, attn, device)
+    from paper_2602_16986_b200 import dist as D
+    bucket = D.GradBucket.for_layer(prm, attn, device)
+    flat, gviews = bucket.flat, bucket.views
     ws_f = U._ws(U.layer_workspace_bytes(jag, m, prm, attn, U.BF16, False), device)
     ws_b = U._ws(U.layer_workspace_bytes(jag, m, prm, attn, U.BF16, True), device)
 
-    def step(xx, dd):
-        U.layer_fwd(jag, m, prm, attn, xx, out=out, ws=ws_f, saved=saved)
-        U.layer_bwd(jag, m, prm, attn, xx, saved, dd, grads=gviews, dx=dx, ws=ws_b)
-        if world > 1:
-            dist.all_reduce(flat)
+    def step(xx, dd):   # one DP training step of the layer on this rank's shard (+ grad all-reduce)
+        D.layer_step(jag, m, prm, attn, xx, dd, bucket, saved=saved, out=out, dx=dx, ws_f=ws_f, ws_b=ws_b)
 
     def barrier():
         if world > 1:
@@ -191,7 +171,6 @@ def run_ours(args, rank, world, local_rank):
     l0 = U.launch_count()
     ms = timed(lambda: step(x, dout), args.steps)
     launches = U.launch_count() - l0
-    clocks = sampler.stop() if sampler else None
     ms_step = ms / args.steps
     total_tokens = T * world if cfg.name == "cfg3" else sum(cfg.lengths)
     value = total_tokens / (ms_step / 1e3)
@@ -215,6 +194,7 @@ def run_ours(args, rank, world, local_rank):
         fa(); fb()
     fwd_ms = timed(fa, args.steps) / args.steps
     bwd_ms = timed(fb, args.steps) / args.steps
+    clocks = sampler.stop() if sampler else None   # sampled across all timed regions
     nnz = U.batch_nnz(jag, m)
     fwd_flop = 4.0 * cfg.dh * cfg.H * nnz
     bwd_flop = 10.0 * cfg.dh * cfg.H * nnz
@@ -330,7 +310,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4"])
