@@ -6,11 +6,15 @@
 //     dV = P^T dA,  dK = alpha dS^T Q,  dQ = alpha dS K,  d rab = scatter-sum of ds.
 // Two kernels, no fp32 atomics on the [T,d] gradients:
 //   dq kernel  (query-major): per 128-query tile, over its visible 64-key tiles:
-//              S, dP (TMEM, double-buffered) -> dS (bf16 smem) -> dQ += dS K (TMEM).
-//              Also reduces d pos_bias / d time_bias (run-length + diagonal sums).
-//   dkv kernel (key-major):   per 128-key tile, over the 64-query tiles that see it:
-//              S^T, dP^T (TMEM, double-buffered) -> P^T, dS^T (bf16 smem)
-//              -> dV += P^T dA, dK += dS^T Q (TMEM).
+//              S = Q K^T, dP = dA V^T with Q, dA as TMEM A operands (tcgen05.cp once per
+//              item); dS (bf16) written over the consumed S columns; dQ += dS K (dS as
+//              TMEM A operand).  Also reduces d pos_bias / d time_bias.
+//   dkv kernel (key-major):   per 128-key tile, over the 32-query tiles that see it:
+//              S^T = K Q^T, dP^T = V dA^T with K, V as TMEM A operands; P^T, dS^T (bf16)
+//              written over the consumed S^T / dP^T columns; dV += P^T dA, dK += dS^T Q.
+// Only K/V (dq) or Q/dA (dkv) tiles cross shared memory per step; TMEM buffers are reused
+// in tensor-pipe order (no "empty" handshakes); the two epilogue warpgroups alternate
+// tiles so one group's MUFU burst overlaps the other's TMEM traffic.
 // Gradients are multiplied by optional gates (silu'(h), the layer's fused
 // "silu_backward") and written straight into their slices of dH (no
 // concat).
@@ -24,23 +28,6 @@ namespace {
 
 constexpr int DH = 128;
 constexpr int NUM_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue
-
-__device__ __forceinline__ void store_bf16_row32(uint8_t* tile, int r, int col0, const float* v) {
-    // row r of a [rows x 64] bf16 K-major SW128 tile; 32 columns starting at col0 (0 or 32)
-    uint8_t* row = tile + r * 128;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int ch = (col0 >> 3) + c;
-        uint4 u = make_uint4(pack_bf16(v[c * 8 + 0], v[c * 8 + 1]), pack_bf16(v[c * 8 + 2], v[c * 8 + 3]),
-                             pack_bf16(v[c * 8 + 4], v[c * 8 + 5]), pack_bf16(v[c * 8 + 6], v[c * 8 + 7]));
-        *reinterpret_cast<uint4*>(row + ((ch ^ (r & 7)) << 4)) = u;
-    }
-}
-
-__device__ __forceinline__ float load_bf16_sw(const uint8_t* tile, int r, int c) {
-    const uint8_t* p = tile + r * 128 + ((((c >> 3) ^ (r & 7))) << 4) + (c & 7) * 2;
-    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p));
-}
 
 __device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t row, int col, const float* v,
                                                 const void* gate, int64_t ldg, float scale) {
@@ -68,52 +55,41 @@ __device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t 
                            pack_bf16(w[ch * 8 + 4], w[ch * 8 + 5]), pack_bf16(w[ch * 8 + 6], w[ch * 8 + 7]));
 }
 
-// bias of 32 consecutive columns: fills b[32]; qpos/kpos of column c = q0c + c*dq, k0c + c*dk
-struct RabRow {
-    const AttnArgs* a;
-    int o;
-};
-
 // ============================================================================ dq kernel
 namespace dq {
 constexpr int BM = 128, BN = 64;
-constexpr int QT = 128 * 128 * 2;       // Q / dA tile bytes (2 x 16K blocks)
-constexpr int KT = 64 * 128 * 2;        // K / V tile bytes (2 x 8K blocks)
-constexpr int ST = 128 * 64 * 2;        // dS tile (1 block)
-constexpr int KV_STAGES = 3;
-constexpr int SMEM = 2 * QT + KV_STAGES * 2 * KT + 2 * ST + kPosTab * 4 + 256 + 1024 + 512;
+constexpr int QT = BM * DH * 2;         // Q / dA tile bytes (2 x 16 KB swizzled blocks)
+constexpr int KT = BN * DH * 2;         // K / V tile bytes (2 x 8 KB blocks)
+constexpr int STAGES = 4;               // (K, V) ring
+constexpr int NS = 2;                   // S / dP buffers in TMEM
+constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256, Q_COL = 384, DA_COL = 448;
+constexpr int SMEM = 2 * QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512;
 
 struct __align__(8) Bars {
     uint64_t qa_full, qa_empty;
-    uint64_t kv_full[KV_STAGES], kv_empty[KV_STAGES];
-    uint64_t s_full[2], s_empty[2];
-    uint64_t ds_full[2], ds_empty[2];
+    uint64_t kv_full[STAGES], kv_empty[STAGES];
+    uint64_t s_full[NS], ds_full[NS];
     uint64_t dq_full, dq_empty;
     uint32_t tmem;
 };
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
     uint8_t* sdA = smem + QT;
-    uint8_t* sK = smem + 2 * QT;                      // [KV_STAGES]
-    uint8_t* sV = sK + KV_STAGES * KT;                // [KV_STAGES]
-    uint8_t* sdS = sV + KV_STAGES * KT;               // [2]
-    float* pos_s = reinterpret_cast<float*>(sdS + 2 * ST);
+    uint8_t* sKV = smem + 2 * QT;                     // [STAGES] x (K 16 KB | V 16 KB)
+    float* pos_s = reinterpret_cast<float*>(sKV + STAGES * 2 * KT);
     float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->qa_full, 1); mbar_init(&bars->qa_empty, 1);
-        for (int i = 0; i < KV_STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bars->s_full[i], 1); mbar_init(&bars->s_empty[i], 8);
-            mbar_init(&bars->ds_full[i], 8); mbar_init(&bars->ds_empty[i], 1);
-        }
+        for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
+        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->ds_full[i], 4); }
         mbar_init(&bars->dq_full, 1); mbar_init(&bars->dq_empty, 8);
         fence_barrier_init();
     }
@@ -125,6 +101,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     const uint32_t tmem = bars->tmem;
 
     if (warp == 0) {
+        // ============================================================ producer
         if (lane == 0) {
             int kc = 0, qi = 0;
             for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
@@ -140,94 +117,99 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 tma_load_2d(sdA + QT / 2, &tmdA, &bars->qa_full, h * DH + 64, it.seq_start + q0);
                 for (int j = 0; j < n; ++j) {
                     const int row = it.seq_start + key_tile_at(kt, j) * BN;
-                    const int s = kc % KV_STAGES;
-                    mbar_wait(&bars->kv_empty[s], ((kc / KV_STAGES) & 1) ^ 1);
+                    const int s = kc % STAGES;
+                    uint8_t* st = sKV + s * 2 * KT;
+                    mbar_wait(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
-                    tma_load_2d(sK + s * KT, &tmK, &bars->kv_full[s], h * DH, row);
-                    tma_load_2d(sK + s * KT + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
-                    tma_load_2d(sV + s * KT, &tmV, &bars->kv_full[s], h * DH, row);
-                    tma_load_2d(sV + s * KT + KT / 2, &tmV, &bars->kv_full[s], h * DH + 64, row);
+                    tma_load_2d(st, &tmK, &bars->kv_full[s], h * DH, row);
+                    tma_load_2d(st + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
+                    tma_load_2d(st + KT, &tmV, &bars->kv_full[s], h * DH, row);
+                    tma_load_2d(st + KT + KT / 2, &tmV, &bars->kv_full[s], h * DH + 64, row);
                     ++kc;
                 }
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // Q x K^T, dA x V^T
-        constexpr uint32_t idesc_q = make_idesc_bf16(BM, DH, false, true);    // dS (K-major) x K (MN-major)
-        int kc = 0, sc = 0, dc = 0, qi = 0;
+        // ============================================================ MMA issuer
+        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [Q|dA](TMEM) x [K|V]^T
+        constexpr uint32_t idesc_q = make_idesc_bf16(BM, DH, false, true);    // dS (TMEM) x K (MN-major)
+        int kc = 0, sc = 0, qi = 0;
         const uint32_t q_addr = smem_u32(sQ), da_addr = smem_u32(sdA);
-        auto issue_dq = [&](int jj, int kstage) {
-            const int db = dc & 1;
-            mbar_wait(&bars->ds_full[db], (dc >> 1) & 1);
-            if (jj == 0) mbar_wait(&bars->dq_empty, (qi & 1) ^ 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t ds_addr = smem_u32(sdS + db * ST);
-                const uint32_t k_addr = smem_u32(sK + kstage * KT);
-#pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk)
-                    umma_ss(tmem + 256, make_sw128_desc(ds_addr + kk * 32, 16, 1024),
-                            make_sw128_desc(k_addr + kk * 2048, KT / 2, 1024), idesc_q, (jj > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&bars->ds_empty[db]);
-                umma_commit(&bars->kv_empty[kstage]);
-            }
-            __syncwarp();
-            ++dc;
-        };
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
             const WorkItem it = a.items[w];
             const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
             const int n = key_tiles_count(kt);
+            const int kc0 = kc, g0 = sc;
             mbar_wait(&bars->qa_full, qi & 1);
-            int prev_stage = 0;
-            for (int j = 0; j < n; ++j) {
-                const int s = kc % KV_STAGES, sb = sc & 1;
-                mbar_wait(&bars->kv_full[s], (kc / KV_STAGES) & 1);
-                mbar_wait(&bars->s_empty[sb], ((sc >> 1) & 1) ^ 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t k_addr = smem_u32(sK + s * KT), v_addr = smem_u32(sV + s * KT);
+            tc_fence_after();
+            if (elect_one()) {   // Q, dA: smem -> TMEM (ordered with the MMAs of the previous item)
 #pragma unroll
-                    for (int kk = 0; kk < DH / 16; ++kk) {
-                        const uint32_t oa = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
-                        const uint32_t ob = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
-                        umma_ss(tmem + sb * BN, make_sw128_desc(q_addr + oa, 16, 1024),
-                                make_sw128_desc(k_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                        umma_ss(tmem + 128 + sb * BN, make_sw128_desc(da_addr + oa, 16, 1024),
-                                make_sw128_desc(v_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                    }
-                    umma_commit(&bars->s_full[sb]);
-                    if (j == n - 1) umma_commit(&bars->qa_empty);
+                for (int kk = 0; kk < DH / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
+                    tmem_cp_128x256b(tmem + Q_COL + kk * 8, make_sw128_desc(q_addr + off, 16, 1024));
+                    tmem_cp_128x256b(tmem + DA_COL + kk * 8, make_sw128_desc(da_addr + off, 16, 1024));
                 }
-                __syncwarp();
-                ++sc;
-                if (j >= 1) issue_dq(j - 1, prev_stage);
-                prev_stage = s;
-                ++kc;
+                umma_commit(&bars->qa_empty);
             }
-            issue_dq(n - 1, prev_stage);
-            if (elect_one()) umma_commit(&bars->dq_full);
             __syncwarp();
+            for (int j = 0; j <= n; ++j) {
+                if (j < n) {   // ---- S(j) = Q K_j^T, dP(j) = dA V_j^T
+                    const int s = kc % STAGES, sb = sc % NS;
+                    mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t k_addr = smem_u32(sKV + s * 2 * KT), v_addr = k_addr + KT;
+#pragma unroll
+                        for (int kk = 0; kk < DH / 16; ++kk) {
+                            const uint32_t ob = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
+                            umma_ts(tmem + S_COL + sb * BN, tmem + Q_COL + kk * 8, make_sw128_desc(k_addr + ob, 16, 1024),
+                                    idesc_s, kk > 0 ? 1u : 0u);
+                            umma_ts(tmem + DP_COL + sb * BN, tmem + DA_COL + kk * 8,
+                                    make_sw128_desc(v_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                        }
+                        umma_commit(&bars->s_full[sb]);
+                    }
+                    __syncwarp();
+                    ++kc; ++sc;
+                }
+                if (j >= 1) {  // ---- dQ += dS(jj) K_jj  (dS over the consumed S columns)
+                    const int jj = j - 1, g = g0 + jj;
+                    const int stage = (kc0 + jj) % STAGES, db = g % NS;
+                    if (jj == 0) mbar_wait(&bars->dq_empty, (qi & 1) ^ 1);
+                    mbar_wait(&bars->ds_full[db], (g / NS) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t k_addr = smem_u32(sKV + stage * 2 * KT);
+#pragma unroll
+                        for (int kk = 0; kk < BN / 16; ++kk)
+                            umma_ts(tmem + DQ_COL, tmem + S_COL + db * BN + (kk >> 1) * 32 + (kk & 1) * 8,
+                                    make_sw128_desc(k_addr + kk * 2048, KT / 2, 1024), idesc_q,
+                                    (jj > 0 || kk > 0) ? 1u : 0u);
+                        umma_commit(&bars->kv_empty[stage]);
+                        if (jj == n - 1) umma_commit(&bars->dq_full);
+                    }
+                    __syncwarp();
+                }
+            }
         }
     } else if (warp >= 4) {
+        // ============================================================ epilogue
         const int wg = (warp - 4) >> 2, wq = warp & 3;
         const int r = wq * 32 + lane;
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const int et = threadIdx.x - 128;  // 0..255 among epilogue threads
         const float ha = 0.5f * a.alpha;
         const float rscale = 0.5f * a.inv_n;   // ds = rscale * ds'  (ds' is what the kernel carries)
-        // d rab partials live in registers / thread-local memory / smem and reach global
-        // memory once per CTA (same-address global atomics from every row would serialise)
+        // d rab partials live in registers / thread-local memory and reach global memory once
+        // per CTA (same-address global atomics from every row would serialise)
         float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals), in ds' units
-        // near diagonals: tile offsets are multiples of 32, so this lane only ever meets
-        // diagonals lane + 32 t; their partial sums stay in registers (P <= 256 -> t < 8)
-        float dpr[kMaxNearT];
+        float dpr[kMaxNearT];      // near diagonals lane + 32 t (tile offsets are multiples of 32)
 #pragma unroll
         for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
         float ts_acc[32];          // d time_bias per bucket, this thread's rows
 #pragma unroll
         for (int b = 0; b < 32; ++b) ts_acc[b] = 0.f;
-        int sc = 0, dc = 0, qi = 0;
+        int sc = 0, qi = 0;
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
             const WorkItem it = a.items[w];
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
@@ -240,119 +222,113 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
             int cur_b = -1;            // d time_bias run-length state (buckets are monotone along the row)
             float cur_acc = 0.f;
-            int32_t tnext = col_time(cx, key_tile_at(kt, 0) * BN + wg * 32, lane);
-            for (int j = 0; j < n; ++j) {
+            auto run_add = [&](int bb, float v) {
+                if (bb != cur_b) {
+                    if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
+                    cur_b = bb; cur_acc = 0.f;
+                }
+                cur_acc += v;
+            };
+            for (int j = 0; j < n; ++j, ++sc) {
+                if ((sc & 1) != wg) continue;       // tiles alternate between the warpgroups
+                const int sb = sc % NS;
                 const int k0 = key_tile_at(kt, j) * BN;
-                const int kb = k0 + wg * 32;
-                const int32_t tcur = tnext;
-                if (j + 1 < n) tnext = col_time(cx, key_tile_at(kt, j + 1) * BN + wg * 32, lane);
-                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, tcur);
-                const int sb = sc & 1;
-                mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
+                const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
+                mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
-                float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + sb * BN + wg * 32, sv);
-                tmem_ld32(tmem + lane_base + 128 + sb * BN + wg * 32, dp);
-                tmem_ld_wait();
+#pragma unroll
+                for (int hc = 0; hc < 2; ++hc) {
+                    const int kb = k0 + 32 * hc;
+                    const Chunk ch = q_chunk(cx, qp, qok, tq, kb, hc ? tc1 : tc0);
+                    float sv[32], dp[32];
+                    tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * hc, sv);
+                    tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * hc, dp);
+                    tmem_ld_wait();
+                    // ds' = dP (1 + t)(1 + h (1 - t)), h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
+                    float hx[32];
+                    int bk[32];
+                    q_h<true>(cx, ch, tq, sv, hx, bk);
+                    uint32_t d2[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
+                        const uint32_t t2 = tanh_bf16x2(h2);
+                        const uint32_t a1 = add_bf16x2(t2, kBf16One2);
+                        const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
+                        d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
+                    }
+                    if (ch.flags & FLAG_M) {
+#pragma unroll
+                        for (int c = 0; c < 32; ++c)
+                            if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2, c);
+                    }
+                    if (!qok) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) d2[i] = 0u;
+                    }
+                    // dS -> TMEM over this chunk's consumed S columns (A operand of dQ += dS K)
+                    tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * hc, d2);
+                    // ---- d rab partials (fp32 accumulation of the bf16 ds')
+                    if (a.dpos || a.dts) {
+                        const float tsum = sum_packed16(d2);
+                        if (a.dts && qok) {
+                            if (ch.b_other == ch.b_base) {
+                                run_add(ch.b_base, tsum);
+                            } else if (ch.b_other == ch.b_base + 1) {
+                                uint32_t m2[16];
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
+                                const float so = sum_packed16(m2);
+                                run_add(ch.b_other, so);
+                                run_add(ch.b_base, tsum - so);
+                            } else {
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) {
+                                    const float2 u = unpack_bf16x2(d2[c >> 1]);
+                                    run_add(bk[c], (c & 1) ? u.y : u.x);
+                                }
+                            }
+                        }
+                        far_acc += tsum;
+                        // near diagonals (delta <= P-2): delta = C + lane - c with C a multiple of 32;
+                        // a skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
+                        if (a.dpos) {
+                            const int C = q0 - kb + 32 * wq;
+                            if (C >= -31 && C <= a.P + 29) {   // warp-uniform
+                                float lo_s = 0.f, hi_s = 0.f;
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) {
+                                    const float2 u =
+                                        unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (lane + c) & 31));
+                                    const float xv = (c & 1) ? u.y : u.x;
+                                    if (lane + c < 32) lo_s += xv; else hi_s += xv;
+                                }
+                                const int dlo = C + lane, dhi = C + lane - 32;
+                                const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
+                                const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
+#pragma unroll
+                                for (int t = 0; t < kMaxNearT; ++t) {
+                                    dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
+                                    dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
+                                }
+                                far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
+                            }
+                        }
+                    }
+                }
+                tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
-                ++sc;
-                // ds' = dP (1 + t)(1 + h (1 - t)),  h = x/2, t = tanh(h)  ==  2 N ds
-                // ds' = dP (1 + t)(1 + h (1 - t)),  h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
-                float hx[32];
-                int bk[32];
-                q_h<true>(cx, ch, tq, sv, hx, bk);
-                uint32_t d2[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
-                    const uint32_t t2 = tanh_bf16x2(h2);
-                    const uint32_t a1 = add_bf16x2(t2, kBf16One2);
-                    const uint32_t w = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
-                    d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, w));
-                }
-                if (ch.flags & FLAG_M) {
-#pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2, c);
-                }
-                if (!qok) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) d2[i] = 0u;
-                }
-                // ---- d rab partials (fp32 accumulation of the bf16 ds')
-                if (a.dpos || a.dts) {
-                    const float tsum = sum_packed16(d2);
-                    if (a.dts && qok) {
-                        auto run_add = [&](int bb, float v) {
-                            if (bb != cur_b) {
-                                if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
-                                cur_b = bb; cur_acc = 0.f;
-                            }
-                            cur_acc += v;
-                        };
-                        if (ch.b_other == ch.b_base) {
-                            run_add(ch.b_base, tsum);
-                        } else if (ch.b_other == ch.b_base + 1) {
-                            uint32_t m2[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
-                            const float so = sum_packed16(m2);
-                            run_add(ch.b_other, so);
-                            run_add(ch.b_base, tsum - so);
-                        } else {
-#pragma unroll
-                            for (int c = 0; c < 32; ++c) {
-                                const float2 u = unpack_bf16x2(d2[c >> 1]);
-                                run_add(bk[c], (c & 1) ? u.y : u.x);
-                            }
-                        }
-                    }
-                    far_acc += tsum;
-                    // d pos_bias near diagonals (delta <= P-2): delta = C + lane - c with C a multiple of 32;
-                    // a skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
-                    if (a.dpos) {
-                        const int C = q0 - k0 + 32 * (wq - wg);
-                        if (C >= -31 && C <= a.P + 29) {   // warp-uniform
-                            float lo_s = 0.f, hi_s = 0.f;
-#pragma unroll
-                            for (int c = 0; c < 32; ++c) {
-                                const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (lane + c) & 31));
-                                const float xv = (c & 1) ? u.y : u.x;
-                                if (lane + c < 32) lo_s += xv; else hi_s += xv;
-                            }
-                            const int dlo = C + lane, dhi = C + lane - 32;
-                            const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
-                            const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
-#pragma unroll
-                            for (int t = 0; t < kMaxNearT; ++t) {
-                                dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
-                                dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
-                            }
-                            far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
-                        }
-                    }
-                }
-                // ---- dS' (bf16) -> smem for dQ += dS K
-                const int db = dc & 1;
-                mbar_wait(&bars->ds_empty[db], ((dc >> 1) & 1) ^ 1);
-                uint8_t* tile = sdS + db * ST;
-                store_row32_packed(tile, r, wg * 32, d2);
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->ds_full[db]);
-                ++dc;
+                if (lane == 0) mbar_arrive(&bars->ds_full[sb]);
             }
-            // ---- close this item's time-bucket run
-            if (a.dts && cur_b >= 0) ts_acc[cur_b] += cur_acc;
+            if (a.dts && cur_b >= 0) ts_acc[cur_b] += cur_acc;   // close this item's run
             // ---- dQ epilogue: dQ = alpha/(2N) * (dS' K)
             mbar_wait(&bars->dq_full, qi & 1);
             tc_fence_after();
             float v[64];
-            tmem_ld32(tmem + lane_base + 256 + wg * 64, v);
-            tmem_ld32(tmem + lane_base + 256 + wg * 64 + 32, v + 32);
+            tmem_ld32(tmem + lane_base + DQ_COL + wg * 64, v);
+            tmem_ld32(tmem + lane_base + DQ_COL + wg * 64 + 32, v + 32);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
@@ -361,7 +337,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         }
         // ---- CTA-level reduction of the d rab partials, then one global atomic per entry
         if (a.dpos || a.dts) {
-            float* red = reinterpret_cast<float*>(sQ);          // Q/dA tiles are no longer in use
+            float* red = reinterpret_cast<float*>(sQ);          // Q/dA staging is no longer in use
             named_bar_sync(2, 256);
             if (a.dts) {
 #pragma unroll
@@ -406,49 +382,44 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 
 // ============================================================================ dkv kernel
 namespace dkv {
-constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per tile
-constexpr int KT = 128 * 128 * 2;         // K / V tile bytes
-constexpr int QT = 64 * 128 * 2;          // Q / dA tile bytes
-constexpr int PT = 128 * 64 * 2;          // P^T / dS^T tile bytes
-constexpr int QA_STAGES = 3;
-constexpr int SMEM = 2 * KT + QA_STAGES * 2 * QT + 2 * PT + kPosTab * 4 + 256 + 1024 + 512;
+constexpr int BM = 128, BN = 32;          // 128 keys (MMA M), 32 queries per step
+constexpr int KT = BM * DH * 2;           // K / V staging tile (32 KB)
+constexpr int QT = BN * DH * 2;           // Q / dA tile (8 KB: 2 x 4 KB blocks of [32 rows x 128 B])
+constexpr int STAGES = 6;                 // (Q, dA) ring
+constexpr int NS = 2;                     // S^T / dP^T buffers
+constexpr int K_COL = 0, V_COL = 64, S_COL = 128, DP_COL = 192, DV_COL = 256, DK_COL = 384;
+constexpr int SMEM = 2 * KT + STAGES * 2 * QT + kPosTab * 4 + 256 + 1024 + 512;
 
 struct __align__(8) Bars {
     uint64_t kv_full, kv_empty;
-    uint64_t qa_full[QA_STAGES], qa_empty[QA_STAGES];
-    uint64_t s_full[2], s_empty[2];
-    uint64_t p_full, p_empty;
+    uint64_t qa_full[STAGES], qa_empty[STAGES];
+    uint64_t s_full[NS], p_full[NS];
     uint64_t acc_full, acc_empty;
     uint32_t tmem;
 };
 
 __device__ __forceinline__ int n_qtiles(int k0, int L, int K1, int K2) {
     const int qe = query_end(k0, BM, L, K1, K2);
-    const int first = k0 / BN;
-    return (qe + BN - 1) / BN - first;
+    return (qe + BN - 1) / BN - k0 / BN;
 }
 
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;
     uint8_t* sV = smem + KT;
-    uint8_t* sQ = smem + 2 * KT;                 // [QA_STAGES]
-    uint8_t* sdA = sQ + QA_STAGES * QT;          // [QA_STAGES]
-    uint8_t* sP = sdA + QA_STAGES * QT;
-    uint8_t* sdS = sP + PT;
-    float* pos_s = reinterpret_cast<float*>(sdS + PT);
+    uint8_t* sQA = smem + 2 * KT;                 // [STAGES] x (Q 8 KB | dA 8 KB)
+    float* pos_s = reinterpret_cast<float*>(sQA + STAGES * 2 * QT);
     float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1); mbar_init(&bars->kv_empty, 1);
-        for (int i = 0; i < QA_STAGES; ++i) { mbar_init(&bars->qa_full[i], 1); mbar_init(&bars->qa_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->s_empty[i], 8); }
-        mbar_init(&bars->p_full, 8); mbar_init(&bars->p_empty, 1);
+        for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->qa_full[i], 1); mbar_init(&bars->qa_empty[i], 1); }
+        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 4); }
         mbar_init(&bars->acc_full, 1); mbar_init(&bars->acc_empty, 8);
         fence_barrier_init();
     }
@@ -460,6 +431,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     const uint32_t tmem = bars->tmem;
 
     if (warp == 0) {
+        // ============================================================ producer
         if (lane == 0) {
             int qc = 0, ki = 0;
             for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
@@ -474,82 +446,91 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tma_load_2d(sV + KT / 2, &tmV, &bars->kv_full, h * DH + 64, it.seq_start + k0);
                 for (int i = 0; i < n; ++i) {
                     const int row = it.seq_start + (k0 / BN + i) * BN;
-                    const int s = qc % QA_STAGES;
-                    mbar_wait(&bars->qa_empty[s], ((qc / QA_STAGES) & 1) ^ 1);
+                    const int s = qc % STAGES;
+                    uint8_t* st = sQA + s * 2 * QT;
+                    mbar_wait(&bars->qa_empty[s], ((qc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(&bars->qa_full[s], 2 * QT);
-                    tma_load_2d(sQ + s * QT, &tmQ, &bars->qa_full[s], h * DH, row);
-                    tma_load_2d(sQ + s * QT + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
-                    tma_load_2d(sdA + s * QT, &tmdA, &bars->qa_full[s], h * DH, row);
-                    tma_load_2d(sdA + s * QT + QT / 2, &tmdA, &bars->qa_full[s], h * DH + 64, row);
+                    tma_load_2d(st, &tmQ, &bars->qa_full[s], h * DH, row);
+                    tma_load_2d(st + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
+                    tma_load_2d(st + QT, &tmdA, &bars->qa_full[s], h * DH, row);
+                    tma_load_2d(st + QT + QT / 2, &tmdA, &bars->qa_full[s], h * DH + 64, row);
                     ++qc;
                 }
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // K x Q^T, V x dA^T
-        constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // P^T (K-major) x dA (MN-major)
-        int qc = 0, sc = 0, pc = 0, ki = 0;
+        // ============================================================ MMA issuer
+        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [K|V](TMEM) x [Q|dA]^T
+        constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // [P^T|dS^T](TMEM) x [dA|Q] (MN-major)
+        int qc = 0, sc = 0, ki = 0;
         const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-        auto issue_acc = [&](int ii, int st) {
-            mbar_wait(&bars->p_full, pc & 1);
-            if (ii == 0) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t p_addr = smem_u32(sP), ds_addr = smem_u32(sdS);
-                const uint32_t da_addr = smem_u32(sdA + st * QT), q_addr = smem_u32(sQ + st * QT);
-#pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk) {
-                    umma_ss(tmem + 256, make_sw128_desc(p_addr + kk * 32, 16, 1024),
-                            make_sw128_desc(da_addr + kk * 2048, QT / 2, 1024), idesc_a, (ii > 0 || kk > 0) ? 1u : 0u);
-                    umma_ss(tmem + 384, make_sw128_desc(ds_addr + kk * 32, 16, 1024),
-                            make_sw128_desc(q_addr + kk * 2048, QT / 2, 1024), idesc_a, (ii > 0 || kk > 0) ? 1u : 0u);
-                }
-                umma_commit(&bars->p_empty);
-                umma_commit(&bars->qa_empty[st]);
-            }
-            __syncwarp();
-            ++pc;
-        };
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
             const WorkItem it = a.items[w];
             const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+            const int qc0 = qc, g0 = sc;
             mbar_wait(&bars->kv_full, ki & 1);
-            int prev = 0;
-            for (int i = 0; i < n; ++i) {
-                const int s = qc % QA_STAGES, sb = sc & 1;
-                mbar_wait(&bars->qa_full[s], (qc / QA_STAGES) & 1);
-                mbar_wait(&bars->s_empty[sb], ((sc >> 1) & 1) ^ 1);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t q_addr = smem_u32(sQ + s * QT), da_addr = smem_u32(sdA + s * QT);
+            tc_fence_after();
+            if (elect_one()) {   // K, V: smem -> TMEM (A operands of S^T, dP^T)
 #pragma unroll
-                    for (int kk = 0; kk < DH / 16; ++kk) {
-                        const uint32_t oa = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
-                        const uint32_t ob = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
-                        umma_ss(tmem + sb * BN, make_sw128_desc(k_addr + oa, 16, 1024),
-                                make_sw128_desc(q_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                        umma_ss(tmem + 128 + sb * BN, make_sw128_desc(v_addr + oa, 16, 1024),
-                                make_sw128_desc(da_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                    }
-                    umma_commit(&bars->s_full[sb]);
-                    if (i == n - 1) umma_commit(&bars->kv_empty);
+                for (int kk = 0; kk < DH / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
+                    tmem_cp_128x256b(tmem + K_COL + kk * 8, make_sw128_desc(k_addr + off, 16, 1024));
+                    tmem_cp_128x256b(tmem + V_COL + kk * 8, make_sw128_desc(v_addr + off, 16, 1024));
                 }
-                __syncwarp();
-                ++sc;
-                if (i >= 1) issue_acc(i - 1, prev);
-                prev = s;
-                ++qc;
+                umma_commit(&bars->kv_empty);
             }
-            issue_acc(n - 1, prev);
-            if (elect_one()) umma_commit(&bars->acc_full);
             __syncwarp();
+            for (int i = 0; i <= n; ++i) {
+                if (i < n) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
+                    const int s = qc % STAGES, sb = sc % NS;
+                    mbar_wait(&bars->qa_full[s], (qc / STAGES) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t q_addr = smem_u32(sQA + s * 2 * QT), da_addr = q_addr + QT;
+#pragma unroll
+                        for (int kk = 0; kk < DH / 16; ++kk) {
+                            const uint32_t ob = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
+                            umma_ts(tmem + S_COL + sb * BN, tmem + K_COL + kk * 8, make_sw128_desc(q_addr + ob, 16, 1024),
+                                    idesc_s, kk > 0 ? 1u : 0u);
+                            umma_ts(tmem + DP_COL + sb * BN, tmem + V_COL + kk * 8,
+                                    make_sw128_desc(da_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+                        }
+                        umma_commit(&bars->s_full[sb]);
+                    }
+                    __syncwarp();
+                    ++qc; ++sc;
+                }
+                if (i >= 1) {  // ---- dV += P^T(ii) dA_ii, dK += dS^T(ii) Q_ii (P^T, dS^T over consumed columns)
+                    const int ii = i - 1, g = g0 + ii;
+                    const int stage = (qc0 + ii) % STAGES, pb = g % NS;
+                    if (ii == 0) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
+                    mbar_wait(&bars->p_full[pb], (g / NS) & 1);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t q_addr = smem_u32(sQA + stage * 2 * QT), da_addr = q_addr + QT;
+#pragma unroll
+                        for (int kk = 0; kk < BN / 16; ++kk) {
+                            umma_ts(tmem + DV_COL, tmem + S_COL + pb * BN + kk * 8,
+                                    make_sw128_desc(da_addr + kk * 2048, QT / 2, 1024), idesc_a,
+                                    (ii > 0 || kk > 0) ? 1u : 0u);
+                            umma_ts(tmem + DK_COL, tmem + DP_COL + pb * BN + kk * 8,
+                                    make_sw128_desc(q_addr + kk * 2048, QT / 2, 1024), idesc_a,
+                                    (ii > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        umma_commit(&bars->qa_empty[stage]);
+                        if (ii == n - 1) umma_commit(&bars->acc_full);
+                    }
+                    __syncwarp();
+                }
+            }
         }
     } else if (warp >= 4) {
+        // ============================================================ epilogue
         const int wg = (warp - 4) >> 2, wq = warp & 3;
         const int r = wq * 32 + lane;
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const float ha = 0.5f * a.alpha;
-        int sc = 0, pc = 0, ki = 0;
+        int sc = 0, ki = 0;
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
             const WorkItem it = a.items[w];
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
@@ -559,57 +540,52 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const bool kok = kp < L;
             const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
             const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
-            int32_t tnext = col_time(cx, (k0 / BN) * BN + wg * 32, lane);
-            for (int i = 0; i < n; ++i) {
-                const int qb = (k0 / BN + i) * BN + wg * 32;
-                const int32_t tcur = tnext;
-                if (i + 1 < n) tnext = col_time(cx, (k0 / BN + i + 1) * BN + wg * 32, lane);
+            for (int i = 0; i < n; ++i, ++sc) {
+                if ((sc & 1) != wg) continue;       // q tiles alternate between the warpgroups
+                const int sb = sc % NS;
+                const int qb = (k0 / BN + i) * BN;
+                const int32_t tcur = col_time(cx, qb, lane);
                 const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
-                const int sb = sc & 1;
-                mbar_wait(&bars->s_full[sb], (sc >> 1) & 1);
+                mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
                 float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + sb * BN + wg * 32, sv);
-                tmem_ld32(tmem + lane_base + 128 + sb * BN + wg * 32, dp);
+                tmem_ld32(tmem + lane_base + S_COL + sb * BN, sv);
+                tmem_ld32(tmem + lane_base + DP_COL + sb * BN, dp);
                 tmem_ld_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->s_empty[sb]);
-                ++sc;
-                // p' = silu(x) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  h = x/2, t = tanh(h)
                 // p' = silu(2h) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  t = tanh(h); bf16x2
                 float hx[32];
                 k_h(cx, ch, tk, sv, hx);
                 uint32_t p2[16], d2[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
+                for (int c = 0; c < 16; ++c) {
+                    const uint32_t h2 = pack_bf16(hx[2 * c], hx[2 * c + 1]);
                     const uint32_t t2 = tanh_bf16x2(h2);
                     const uint32_t a1 = add_bf16x2(t2, kBf16One2);
-                    p2[i] = mul_bf16x2(h2, a1);
-                    const uint32_t w = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
-                    d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, w));
+                    p2[c] = mul_bf16x2(h2, a1);
+                    const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
+                    d2[c] = mul_bf16x2(pack_bf16(dp[2 * c], dp[2 * c + 1]), mul_bf16x2(a1, wv));
                 }
                 if (ch.flags & FLAG_M) {
 #pragma unroll
                     for (int c = 0; c < 32; ++c)
                         if (!k_visible(cx, kp, kok, qb + c)) { zero_half(p2, c); zero_half(d2, c); }
                 }
-                mbar_wait(&bars->p_empty, (pc & 1) ^ 1);
-                store_row32_packed(sP, r, wg * 32, p2);
-                store_row32_packed(sdS, r, wg * 32, d2);
-                fence_proxy_async_smem();
+                // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
+                tmem_st16(tmem + lane_base + S_COL + sb * BN, p2);
+                tmem_st16(tmem + lane_base + DP_COL + sb * BN, d2);
+                tmem_st_wait();
+                tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->p_full);
-                ++pc;
+                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+                if (lane == 0) TRACE((warp - 4) * 1024 + (sc & 1023));
             }
             mbar_wait(&bars->acc_full, ki & 1);
             tc_fence_after();
             float dv[64], dk[64];
-            tmem_ld32(tmem + lane_base + 256 + wg * 64, dv);
-            tmem_ld32(tmem + lane_base + 256 + wg * 64 + 32, dv + 32);
-            tmem_ld32(tmem + lane_base + 384 + wg * 64, dk);
-            tmem_ld32(tmem + lane_base + 384 + wg * 64 + 32, dk + 32);
+            tmem_ld32(tmem + lane_base + DV_COL + wg * 64, dv);
+            tmem_ld32(tmem + lane_base + DV_COL + wg * 64 + 32, dv + 32);
+            tmem_ld32(tmem + lane_base + DK_COL + wg * 64, dk);
+            tmem_ld32(tmem + lane_base + DK_COL + wg * 64 + 32, dk + 32);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
@@ -642,16 +618,22 @@ uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStr
     note_launch();
     UH_CUDA(cudaGetLastError());
 
-    CUtensorMap q64, dA64, k128, v128;
-    UH_TRY(make_tmap_bf16(&q64, akv.q, width, T, akv.ld_qkv, 64, 64));
-    UH_TRY(make_tmap_bf16(&dA64, akv.dout, width, T, akv.ld_dout, 64, 64));
+    CUtensorMap q32, dA32, k128, v128;
+    UH_TRY(make_tmap_bf16(&q32, akv.q, width, T, akv.ld_qkv, 64, dkv::BN));
+    UH_TRY(make_tmap_bf16(&dA32, akv.dout, width, T, akv.ld_dout, 64, dkv::BN));
     UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));
     UH_TRY(make_tmap_bf16(&v128, akv.v, width, T, akv.ld_qkv, 64, 128));
     UH_CUDA(cudaFuncSetAttribute(dkv::attn_bwd_dkv_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv::SMEM));
-    dkv::attn_bwd_dkv_sm100<<<akv.n_items < sms ? akv.n_items : sms, NUM_THREADS, dkv::SMEM, st>>>(q64, k128, v128, dA64, akv);
+    dkv::attn_bwd_dkv_sm100<<<akv.n_items < sms ? akv.n_items : sms, NUM_THREADS, dkv::SMEM, st>>>(q32, k128, v128, dA32, akv);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
 }
 
 }  // namespace uh
+
+#if UH_TRACE
+extern "C" __attribute__((visibility("default"))) int uh_trace_set_bwd(long long* p) {
+    return (int)cudaMemcpyToSymbol(uh::g_trace, &p, sizeof(p));
+}
+#endif

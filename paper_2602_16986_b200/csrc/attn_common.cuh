@@ -8,6 +8,14 @@
 
 namespace uh {
 
+#if UH_TRACE
+// timestamps of CTA 0 for timeline analysis (trace builds only: -DUH_TRACE=1)
+__device__ long long* g_trace = nullptr;
+#define TRACE(slot) do { if (blockIdx.x == 0 && g_trace && (slot) < 8192) g_trace[(slot)] = clock64(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
+
 #define UH_HD __host__ __device__ __forceinline__
 UH_HD int imin(int a, int b) { return a < b ? a : b; }
 UH_HD int imax(int a, int b) { return a > b ? a : b; }

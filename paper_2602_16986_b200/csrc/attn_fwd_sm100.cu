@@ -25,12 +25,6 @@
 #include "internal.h"
 
 namespace uh {
-#if UH_TRACE
-__device__ long long* g_trace = nullptr;   // [role][event] timestamps of CTA 0 (trace builds only)
-#define TRACE(slot) do { if (blockIdx.x == 0 && g_trace && (slot) < 8192) g_trace[(slot)] = clock64(); } while (0)
-#else
-#define TRACE(slot) do { } while (0)
-#endif
 namespace {
 
 constexpr int BM = 128, BN = 64, DH = 128;
