@@ -63,7 +63,7 @@ constexpr int KT = BN * DH * 2;         // K / V tile bytes (2 x 8 KB blocks)
 constexpr int STAGES = 4;               // (K, V) ring
 constexpr int NS = 2;                   // S / dP buffers in TMEM
 constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256, Q_COL = 384, DA_COL = 448;
-constexpr int SMEM = 2 * QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512;
+constexpr int SMEM = 2 * QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512 + 1024;
 
 struct __align__(8) Bars {
     uint64_t qa_full, qa_empty;
@@ -85,6 +85,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TRACE_SETUP();
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->qa_full, 1); mbar_init(&bars->qa_empty, 1);
@@ -94,6 +95,8 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
+    float* tsw = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);   // [8 warps][32] d time_bias
+    if (threadIdx.x < 256) tsw[threadIdx.x] = 0.f;
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
@@ -200,15 +203,12 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         const int et = threadIdx.x - 128;  // 0..255 among epilogue threads
         const float ha = 0.5f * a.alpha;
         const float rscale = 0.5f * a.inv_n;   // ds = rscale * ds'  (ds' is what the kernel carries)
-        // d rab partials live in registers / thread-local memory and reach global memory once
+        // d rab partials live in registers / per-warp shared rows and reach global memory once
         // per CTA (same-address global atomics from every row would serialise)
         float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals), in ds' units
         float dpr[kMaxNearT];      // near diagonals lane + 32 t (tile offsets are multiples of 32)
 #pragma unroll
         for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
-        float ts_acc[32];          // d time_bias per bucket, this thread's rows
-#pragma unroll
-        for (int b = 0; b < 32; ++b) ts_acc[b] = 0.f;
         int sc = 0, qi = 0;
         for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
             const WorkItem it = a.items[w];
@@ -220,14 +220,79 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const bool qok = qp < L;
             const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
-            int cur_b = -1;            // d time_bias run-length state (buckets are monotone along the row)
-            float cur_acc = 0.f;
-            auto run_add = [&](int bb, float v) {
-                if (bb != cur_b) {
-                    if (cur_b >= 0) ts_acc[cur_b] += cur_acc;
-                    cur_b = bb; cur_acc = 0.f;
+            // d rab partials of one 32-column chunk; runs after ds_full (off the S -> dS -> next-S
+            // chain, overlapping the tensor pipe).  d time_bias: lanes grouped by bucket, a warp
+            // sum, one lane adds into this warp's shared row (no atomics, no local memory).
+            float* const tsw_w = tsw + (warp - 4) * 32;
+            auto bucket_add = [&](int bb, float v) {   // bb per lane (-1: none)
+                unsigned pend = __ballot_sync(0xffffffffu, bb >= 0);
+                while (pend) {
+                    const int lb = __shfl_sync(0xffffffffu, bb, __ffs(pend) - 1);
+                    const bool mine = bb == lb;
+                    float x = mine ? v : 0.f;
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+                    if (lane == 0) tsw_w[lb] += x;
+                    pend &= ~__ballot_sync(0xffffffffu, mine);
                 }
-                cur_acc += v;
+            };
+            auto rab_grads = [&](const Chunk& ch, const uint32_t* d2, int kb) {
+                const float tsum = sum_packed16(d2);   // rows beyond L carry zeros
+                if (a.dts) {
+                    if (!(ch.flags & FLAG_T2)) {
+                        float so = 0.f;                // columns [0, n) are in bucket b_other (FLAG_T1)
+                        if (ch.flags & FLAG_T1) {
+                            uint32_t m2[16];
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
+                            so = sum_packed16(m2);
+                            bucket_add(qok && ch.n > 0 ? ch.b_other : -1, so);
+                        }
+                        bucket_add(qok ? ch.b_base : -1, tsum - so);
+                    } else {                           // next to the diagonal: per-element buckets
+                        int bk[32];
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) bk[c] = bucket32(tq - __shfl_sync(0xffffffffu, ch.tcol, c), cx.NB);
+                        const int lo = __reduce_min_sync(0xffffffffu, qok ? ch.b_base : 64);
+                        const int hi = __reduce_max_sync(0xffffffffu, qok ? ch.b_other : -1);
+                        for (int bb = lo; bb <= hi; ++bb) {   // warp-uniform
+                            float x = 0.f;
+#pragma unroll
+                            for (int c = 0; c < 32; ++c) {
+                                const float2 u = unpack_bf16x2(d2[c >> 1]);
+                                x += bk[c] == bb ? ((c & 1) ? u.y : u.x) : 0.f;
+                            }
+#pragma unroll
+                            for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+                            if (lane == 0) tsw_w[bb] += x;
+                        }
+                    }
+                }
+                far_acc += tsum;
+                // near diagonals (delta <= P-2): delta = C + lane - c with C a multiple of 32;
+                // a skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
+                if (a.dpos) {
+                    const int C = q0 - kb + 32 * wq;
+                    if (C >= -31 && C <= a.P + 29) {   // warp-uniform
+                        float lo_s = 0.f, hi_s = 0.f;
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {
+                            const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (lane + c) & 31));
+                            const float xv = (c & 1) ? u.y : u.x;
+                            if (lane + c < 32) lo_s += xv; else hi_s += xv;
+                        }
+                        const int dlo = C + lane, dhi = C + lane - 32;
+                        const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
+                        const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
+#pragma unroll
+                        for (int t = 0; t < kMaxNearT; ++t) {
+                            dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
+                            dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
+                        }
+                        far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
+                    }
+                }
             };
             for (int j = 0; j < n; ++j, ++sc) {
                 if ((sc & 1) != wg) continue;       // tiles alternate between the warpgroups
@@ -236,93 +301,49 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
                 mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
+                Chunk chs[2];
+                uint32_t d2[2][16];
 #pragma unroll
                 for (int hc = 0; hc < 2; ++hc) {
                     const int kb = k0 + 32 * hc;
-                    const Chunk ch = q_chunk(cx, qp, qok, tq, kb, hc ? tc1 : tc0);
+                    chs[hc] = q_chunk(cx, qp, qok, tq, kb, hc ? tc1 : tc0);
+                    const Chunk& ch = chs[hc];
                     float sv[32], dp[32];
                     tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * hc, sv);
                     tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * hc, dp);
                     tmem_ld_wait();
                     // ds' = dP (1 + t)(1 + h (1 - t)), h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
                     float hx[32];
-                    int bk[32];
-                    q_h<true>(cx, ch, tq, sv, hx, bk);
-                    uint32_t d2[16];
+                    q_h<false>(cx, ch, tq, sv, hx, nullptr);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
                         const uint32_t t2 = tanh_bf16x2(h2);
                         const uint32_t a1 = add_bf16x2(t2, kBf16One2);
                         const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
-                        d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
+                        d2[hc][i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
                     }
                     if (ch.flags & FLAG_M) {
 #pragma unroll
                         for (int c = 0; c < 32; ++c)
-                            if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2, c);
+                            if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2[hc], c);
                     }
                     if (!qok) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) d2[i] = 0u;
+                        for (int i = 0; i < 16; ++i) d2[hc][i] = 0u;
                     }
                     // dS -> TMEM over this chunk's consumed S columns (A operand of dQ += dS K)
-                    tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * hc, d2);
-                    // ---- d rab partials (fp32 accumulation of the bf16 ds')
-                    if (a.dpos || a.dts) {
-                        const float tsum = sum_packed16(d2);
-                        if (a.dts && qok) {
-                            if (ch.b_other == ch.b_base) {
-                                run_add(ch.b_base, tsum);
-                            } else if (ch.b_other == ch.b_base + 1) {
-                                uint32_t m2[16];
-#pragma unroll
-                                for (int i = 0; i < 16; ++i)
-                                    m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
-                                const float so = sum_packed16(m2);
-                                run_add(ch.b_other, so);
-                                run_add(ch.b_base, tsum - so);
-                            } else {
-#pragma unroll
-                                for (int c = 0; c < 32; ++c) {
-                                    const float2 u = unpack_bf16x2(d2[c >> 1]);
-                                    run_add(bk[c], (c & 1) ? u.y : u.x);
-                                }
-                            }
-                        }
-                        far_acc += tsum;
-                        // near diagonals (delta <= P-2): delta = C + lane - c with C a multiple of 32;
-                        // a skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
-                        if (a.dpos) {
-                            const int C = q0 - kb + 32 * wq;
-                            if (C >= -31 && C <= a.P + 29) {   // warp-uniform
-                                float lo_s = 0.f, hi_s = 0.f;
-#pragma unroll
-                                for (int c = 0; c < 32; ++c) {
-                                    const float2 u =
-                                        unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (lane + c) & 31));
-                                    const float xv = (c & 1) ? u.y : u.x;
-                                    if (lane + c < 32) lo_s += xv; else hi_s += xv;
-                                }
-                                const int dlo = C + lane, dhi = C + lane - 32;
-                                const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
-                                const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
-#pragma unroll
-                                for (int t = 0; t < kMaxNearT; ++t) {
-                                    dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
-                                    dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
-                                }
-                                far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
-                            }
-                        }
-                    }
+                    tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * hc, d2[hc]);
                 }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_full[sb]);
+                if (a.dpos || a.dts) {
+#pragma unroll
+                    for (int hc = 0; hc < 2; ++hc) rab_grads(chs[hc], d2[hc], k0 + 32 * hc);
+                }
             }
-            if (a.dts && cur_b >= 0) ts_acc[cur_b] += cur_acc;   // close this item's run
             // ---- dQ epilogue: dQ = alpha/(2N) * (dS' K)
             mbar_wait(&bars->dq_full, qi & 1);
             tc_fence_after();
@@ -337,14 +358,8 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         }
         // ---- CTA-level reduction of the d rab partials, then one global atomic per entry
         if (a.dpos || a.dts) {
-            float* red = reinterpret_cast<float*>(sQ);          // Q/dA staging is no longer in use
-            named_bar_sync(2, 256);
-            if (a.dts) {
-#pragma unroll
-                for (int b = 0; b < 32; ++b) red[b * 256 + et] = ts_acc[b];
-            }
-            float* redp = red + 32 * 256;                        // [kMaxNearT*32][8 warps]
-            const int ew = et >> 5;
+            float* redp = reinterpret_cast<float*>(sQ);          // Q/dA staging is no longer in use:
+            const int ew = et >> 5;                              // [kMaxNearT*32][8 warps] + far[8]
             if (a.dpos) {
 #pragma unroll
                 for (int t = 0; t < kMaxNearT; ++t) redp[(t * 32 + lane) * 8 + ew] = dpr[t];
@@ -356,7 +371,8 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             named_bar_sync(2, 256);
             if (a.dts && et < a.NB) {
                 float sum = 0.f;
-                for (int i = 0; i < 256; ++i) sum += red[et * 256 + i];
+#pragma unroll
+                for (int w8 = 0; w8 < 8; ++w8) sum += tsw[w8 * 32 + et];
                 if (sum != 0.f) atomicAdd(a.dts + et, sum * rscale);
             }
             if (a.dpos) {
@@ -415,6 +431,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TRACE_SETUP();
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1); mbar_init(&bars->kv_empty, 1);
@@ -462,65 +479,81 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // ============================================================ MMA issuer
         constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [K|V](TMEM) x [Q|dA]^T
         constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // [P^T|dS^T](TMEM) x [dA|Q] (MN-major)
-        int qc = 0, sc = 0, ki = 0;
-        const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
-            const WorkItem it = a.items[w];
-            const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
-            const int qc0 = qc, g0 = sc;
-            mbar_wait(&bars->kv_full, ki & 1);
-            tc_fence_after();
-            if (elect_one()) {   // K, V: smem -> TMEM (A operands of S^T, dP^T)
+        // The whole warp runs the role convergently (so descriptors live in uniform registers);
+        // one elected lane issues each step's tcgen05.mma block back to back from precomputed
+        // descriptors: at 32 queries per step the issue stream, not the tensor pipe, is the limit.
+        {
+            const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
+            const uint64_t q_k = make_sw128_desc(smem_u32(sQA), 16, 1024);        // Q / dA K-major (S^T, dP^T)
+            const uint64_t q_mn = make_sw128_desc(smem_u32(sQA), QT / 2, 1024);   // Q / dA MN-major (dK, dV)
+            int st_s = 0, ph_s = 0;       // (Q, dA) stage consumed by S^T / dP^T
+            int st_a = 0;                 // stage consumed by dV / dK (trails st_s)
+            int sb = 0, ph_p = 0;         // S buffer of the next S^T; p_full parity of buffer pb
+            int pb = 0;
+            int ki = 0, sc = 0, gc = 0;
+            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+                const WorkItem it = a.items[w];
+                const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+                mbar_wait(&bars->kv_full, ki & 1);
+                tc_fence_after();
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < DH / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
-                    tmem_cp_128x256b(tmem + K_COL + kk * 8, make_sw128_desc(k_addr + off, 16, 1024));
-                    tmem_cp_128x256b(tmem + V_COL + kk * 8, make_sw128_desc(v_addr + off, 16, 1024));
-                }
-                umma_commit(&bars->kv_empty);
-            }
-            __syncwarp();
-            for (int i = 0; i <= n; ++i) {
-                if (i < n) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
-                    const int s = qc % STAGES, sb = sc % NS;
-                    mbar_wait(&bars->qa_full[s], (qc / STAGES) & 1);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t q_addr = smem_u32(sQA + s * 2 * QT), da_addr = q_addr + QT;
-#pragma unroll
-                        for (int kk = 0; kk < DH / 16; ++kk) {
-                            const uint32_t ob = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
-                            umma_ts(tmem + S_COL + sb * BN, tmem + K_COL + kk * 8, make_sw128_desc(q_addr + ob, 16, 1024),
-                                    idesc_s, kk > 0 ? 1u : 0u);
-                            umma_ts(tmem + DP_COL + sb * BN, tmem + V_COL + kk * 8,
-                                    make_sw128_desc(da_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                        }
-                        umma_commit(&bars->s_full[sb]);
+                    for (int kk = 0; kk < DH / 16; ++kk) {   // K, V: smem -> TMEM (A operands of S^T, dP^T)
+                        const uint32_t off = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
+                        tmem_cp_128x256b(tmem + K_COL + kk * 8, make_sw128_desc(k_addr + off, 16, 1024));
+                        tmem_cp_128x256b(tmem + V_COL + kk * 8, make_sw128_desc(v_addr + off, 16, 1024));
                     }
-                    __syncwarp();
-                    ++qc; ++sc;
+                    umma_commit(&bars->kv_empty);
                 }
-                if (i >= 1) {  // ---- dV += P^T(ii) dA_ii, dK += dS^T(ii) Q_ii (P^T, dS^T over consumed columns)
-                    const int ii = i - 1, g = g0 + ii;
-                    const int stage = (qc0 + ii) % STAGES, pb = g % NS;
-                    if (ii == 0) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
-                    mbar_wait(&bars->p_full[pb], (g / NS) & 1);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t q_addr = smem_u32(sQA + stage * 2 * QT), da_addr = q_addr + QT;
+                __syncwarp();
+                for (int i = 0; i <= n; ++i) {
+                    if (i < n) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
+                        if (lane == 0) TRACE(0 * 1024 + (sc & 1023));
+                        mbar_wait(&bars->qa_full[st_s], ph_s);
+                        tc_fence_after();
+                        if (lane == 0) TRACE(1 * 1024 + (sc & 1023));
+                        const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
+                        const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < BN / 16; ++kk) {
-                            umma_ts(tmem + DV_COL, tmem + S_COL + pb * BN + kk * 8,
-                                    make_sw128_desc(da_addr + kk * 2048, QT / 2, 1024), idesc_a,
-                                    (ii > 0 || kk > 0) ? 1u : 0u);
-                            umma_ts(tmem + DK_COL, tmem + DP_COL + pb * BN + kk * 8,
-                                    make_sw128_desc(q_addr + kk * 2048, QT / 2, 1024), idesc_a,
-                                    (ii > 0 || kk > 0) ? 1u : 0u);
+                            for (int kk = 0; kk < DH / 16; ++kk) {
+                                const uint32_t ob = ((kk >> 2) * (QT / 2) + (kk & 3) * 32) >> 4;
+                                umma_ts(d_s, tmem + K_COL + kk * 8, dq + ob, idesc_s, kk > 0 ? 1u : 0u);
+                                umma_ts(d_p, tmem + V_COL + kk * 8, dda + ob, idesc_s, kk > 0 ? 1u : 0u);
+                            }
+                            umma_commit(&bars->s_full[sb]);
                         }
-                        umma_commit(&bars->qa_empty[stage]);
-                        if (ii == n - 1) umma_commit(&bars->acc_full);
+                        __syncwarp();
+                        if (lane == 0) TRACE(2 * 1024 + (sc & 1023));
+                        if (++st_s == STAGES) { st_s = 0; ph_s ^= 1; }
+                        sb ^= 1;
+                        ++sc;
                     }
-                    __syncwarp();
+                    if (i >= 1) {  // ---- dV += P^T dA, dK += dS^T Q (P^T, dS^T over the consumed columns)
+                        if (i == 1) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
+                        if (lane == 0) TRACE(3 * 1024 + (gc & 1023));
+                        mbar_wait(&bars->p_full[pb], ph_p);
+                        tc_fence_after();
+                        if (lane == 0) TRACE(4 * 1024 + (gc & 1023));
+                        const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
+                        const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < BN / 16; ++kk) {
+                                const uint32_t acc = (i > 1 || kk > 0) ? 1u : 0u;
+                                umma_ts(tmem + DV_COL, a_p + kk * 8, dda + kk * (2048 >> 4), idesc_a, acc);
+                                umma_ts(tmem + DK_COL, a_d + kk * 8, dq + kk * (2048 >> 4), idesc_a, acc);
+                            }
+                            umma_commit(&bars->qa_empty[st_a]);
+                            if (i == n) umma_commit(&bars->acc_full);
+                        }
+                        __syncwarp();
+                        if (lane == 0) TRACE(5 * 1024 + (gc & 1023));
+                        if (++st_a == STAGES) st_a = 0;
+                        pb ^= 1;
+                        if (pb == 0) ph_p ^= 1;
+                        ++gc;
+                    }
                 }
             }
         }
@@ -577,7 +610,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
-                if (lane == 0) TRACE((warp - 4) * 1024 + (sc & 1023));
+                if (lane == 0 && (warp & 3) == 0) TRACE((6 + wg) * 1024 + (sc & 1023));
             }
             mbar_wait(&bars->acc_full, ki & 1);
             tc_fence_after();

@@ -11,8 +11,12 @@ namespace uh {
 #if UH_TRACE
 // timestamps of CTA 0 for timeline analysis (trace builds only: -DUH_TRACE=1)
 __device__ long long* g_trace = nullptr;
-#define TRACE(slot) do { if (blockIdx.x == 0 && g_trace && (slot) < 8192) g_trace[(slot)] = clock64(); } while (0)
+// the pointer is read once per kernel into a register: a global load per trace point
+// would add an L2 round trip to every traced interval
+#define TRACE_SETUP() long long* const uh_tr_ = blockIdx.x == 0 ? g_trace : nullptr
+#define TRACE(slot) do { if (uh_tr_ && (slot) < 8192) uh_tr_[(slot)] = clock64(); } while (0)
 #else
+#define TRACE_SETUP() do { } while (0)
 #define TRACE(slot) do { } while (0)
 #endif
 

@@ -14,7 +14,7 @@ from attn_time import run
 run(B=2, rab=bool(int(sys.argv[1])) if len(sys.argv) > 1 else False, steps=1)
 t = buf.view(8, 1024).cpu().numpy()
 t0 = t[t > 0].min()
-names = ["w4", "w5", "w6", "w7", "w8", "w9", "w10", "w11"]
+names = ["s_beg", "s_qa", "s_end", "p_beg", "p_got", "p_end", "wg0_arr", "wg1_arr"]
 for j in range(0, 40):
     row = [(t[e, j] - t0) if t[e, j] > 0 else -1 for e in range(8)]
     print(j, " ".join(f"{n}={v:8d}" for n, v in zip(names, row)))
