@@ -90,7 +90,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     if (threadIdx.x == 0) {
         mbar_init(&bars->qa_full, 1); mbar_init(&bars->qa_empty, 1);
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
-        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->ds_full[i], 4); }
+        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->ds_full[i], 8); }
         mbar_init(&bars->dq_full, 1); mbar_init(&bars->dq_empty, 8);
         fence_barrier_init();
     }
@@ -112,7 +112,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 const int q0 = it.tile * BM, h = it.head & 0xFFFF;
                 const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
                 const int n = key_tiles_count(kt);
-                mbar_wait(&bars->qa_empty, (qi & 1) ^ 1);
+                mbar_wait_sleep(&bars->qa_empty, (qi & 1) ^ 1);
                 mbar_arrive_expect_tx(&bars->qa_full, 2 * QT);
                 tma_load_2d(sQ, &tmQ, &bars->qa_full, h * DH, it.seq_start + q0);
                 tma_load_2d(sQ + QT / 2, &tmQ, &bars->qa_full, h * DH + 64, it.seq_start + q0);
@@ -122,7 +122,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     const int row = it.seq_start + key_tile_at(kt, j) * BN;
                     const int s = kc % STAGES;
                     uint8_t* st = sKV + s * 2 * KT;
-                    mbar_wait(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
+                    mbar_wait_sleep(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
                     tma_load_2d(st, &tmK, &bars->kv_full[s], h * DH, row);
                     tma_load_2d(st + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
@@ -158,8 +158,10 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             for (int j = 0; j <= n; ++j) {
                 if (j < n) {   // ---- S(j) = Q K_j^T, dP(j) = dA V_j^T
                     const int s = kc % STAGES, sb = sc % NS;
+                    if (lane == 0) TRACE(0 * 1024 + (sc & 1023));
                     mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
                     tc_fence_after();
+                    if (lane == 0) TRACE(1 * 1024 + (sc & 1023));
                     if (elect_one()) {
                         const uint32_t k_addr = smem_u32(sKV + s * 2 * KT), v_addr = k_addr + KT;
 #pragma unroll
@@ -179,8 +181,10 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     const int jj = j - 1, g = g0 + jj;
                     const int stage = (kc0 + jj) % STAGES, db = g % NS;
                     if (jj == 0) mbar_wait(&bars->dq_empty, (qi & 1) ^ 1);
+                    if (lane == 0) TRACE(2 * 1024 + (g & 1023));
                     mbar_wait(&bars->ds_full[db], (g / NS) & 1);
                     tc_fence_after();
+                    if (lane == 0) TRACE(3 * 1024 + (g & 1023));
                     if (elect_one()) {
                         const uint32_t k_addr = smem_u32(sKV + stage * 2 * KT);
 #pragma unroll
@@ -294,23 +298,21 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     }
                 }
             };
+            // every tile is split between the warpgroups by column (warpgroup wg: keys
+            // [32 wg, 32 wg + 32)), so tile j+1's epilogue overlaps tile j's dS -> dQ -> S(j+2) chain
             for (int j = 0; j < n; ++j, ++sc) {
-                if ((sc & 1) != wg) continue;       // tiles alternate between the warpgroups
                 const int sb = sc % NS;
-                const int k0 = key_tile_at(kt, j) * BN;
-                const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
-                mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
+                const int kb = key_tile_at(kt, j) * BN + 32 * wg;
+                const int32_t tcw = col_time(cx, kb, lane);
+                mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
-                Chunk chs[2];
-                uint32_t d2[2][16];
-#pragma unroll
-                for (int hc = 0; hc < 2; ++hc) {
-                    const int kb = k0 + 32 * hc;
-                    chs[hc] = q_chunk(cx, qp, qok, tq, kb, hc ? tc1 : tc0);
-                    const Chunk& ch = chs[hc];
+                if ((warp & 3) == 0 && lane == 0) TRACE((4 + wg * 2) * 1024 + (sc & 1023));
+                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, tcw);
+                uint32_t d2[16];
+                {
                     float sv[32], dp[32];
-                    tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * hc, sv);
-                    tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * hc, dp);
+                    tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * wg, sv);
+                    tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * wg, dp);
                     tmem_ld_wait();
                     // ds' = dP (1 + t)(1 + h (1 - t)), h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
                     float hx[32];
@@ -321,31 +323,29 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                         const uint32_t t2 = tanh_bf16x2(h2);
                         const uint32_t a1 = add_bf16x2(t2, kBf16One2);
                         const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
-                        d2[hc][i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
+                        d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
                     }
-                    if (ch.flags & FLAG_M) {
-#pragma unroll
-                        for (int c = 0; c < 32; ++c)
-                            if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2[hc], c);
-                    }
-                    if (!qok) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) d2[hc][i] = 0u;
-                    }
-                    // dS -> TMEM over this chunk's consumed S columns (A operand of dQ += dS K)
-                    tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * hc, d2[hc]);
                 }
+                if (ch.flags & FLAG_M) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2, c);
+                }
+                if (!qok) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) d2[i] = 0u;
+                }
+                // dS -> TMEM over this chunk's consumed S columns (A operand of dQ += dS K)
+                tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, d2);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_full[sb]);
-                if (a.dpos || a.dts) {
-#pragma unroll
-                    for (int hc = 0; hc < 2; ++hc) rab_grads(chs[hc], d2[hc], k0 + 32 * hc);
-                }
+                if ((warp & 3) == 0 && lane == 0) TRACE((5 + wg * 2) * 1024 + (sc & 1023));
+                if (a.dpos || a.dts) rab_grads(ch, d2, kb);
             }
             // ---- dQ epilogue: dQ = alpha/(2N) * (dS' K)
-            mbar_wait(&bars->dq_full, qi & 1);
+            mbar_wait_sleep(&bars->dq_full, qi & 1);
             tc_fence_after();
             float v[64];
             tmem_ld32(tmem + lane_base + DQ_COL + wg * 64, v);
@@ -397,6 +397,11 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 }  // namespace dq
 
 // ============================================================================ dkv kernel
+#if UH_TRACE == 2
+#define TRACE_DKV(x) TRACE(x)
+#else
+#define TRACE_DKV(x) do { } while (0)
+#endif
 namespace dkv {
 constexpr int BM = 128, BN = 32;          // 128 keys (MMA M), 32 queries per step
 constexpr int KT = BM * DH * 2;           // K / V staging tile (32 KB)
@@ -455,7 +460,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 const WorkItem it = a.items[w];
                 const int k0 = it.tile * BM, h = it.head & 0xFFFF;
                 const int n = n_qtiles(k0, it.seq_len, a.K1, a.K2);
-                mbar_wait(&bars->kv_empty, (ki & 1) ^ 1);
+                mbar_wait_sleep(&bars->kv_empty, (ki & 1) ^ 1);
                 mbar_arrive_expect_tx(&bars->kv_full, 2 * KT);
                 tma_load_2d(sK, &tmK, &bars->kv_full, h * DH, it.seq_start + k0);
                 tma_load_2d(sK + KT / 2, &tmK, &bars->kv_full, h * DH + 64, it.seq_start + k0);
@@ -465,7 +470,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     const int row = it.seq_start + (k0 / BN + i) * BN;
                     const int s = qc % STAGES;
                     uint8_t* st = sQA + s * 2 * QT;
-                    mbar_wait(&bars->qa_empty[s], ((qc / STAGES) & 1) ^ 1);
+                    mbar_wait_sleep(&bars->qa_empty[s], ((qc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(&bars->qa_full[s], 2 * QT);
                     tma_load_2d(st, &tmQ, &bars->qa_full[s], h * DH, row);
                     tma_load_2d(st + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
@@ -508,10 +513,10 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 __syncwarp();
                 for (int i = 0; i <= n; ++i) {
                     if (i < n) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
-                        if (lane == 0) TRACE(0 * 1024 + (sc & 1023));
+                        if (lane == 0) TRACE_DKV(0 * 1024 + (sc & 1023));
                         mbar_wait(&bars->qa_full[st_s], ph_s);
                         tc_fence_after();
-                        if (lane == 0) TRACE(1 * 1024 + (sc & 1023));
+                        if (lane == 0) TRACE_DKV(1 * 1024 + (sc & 1023));
                         const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
                         const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
                         if (elect_one()) {
@@ -524,17 +529,17 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                             umma_commit(&bars->s_full[sb]);
                         }
                         __syncwarp();
-                        if (lane == 0) TRACE(2 * 1024 + (sc & 1023));
+                        if (lane == 0) TRACE_DKV(2 * 1024 + (sc & 1023));
                         if (++st_s == STAGES) { st_s = 0; ph_s ^= 1; }
                         sb ^= 1;
                         ++sc;
                     }
                     if (i >= 1) {  // ---- dV += P^T dA, dK += dS^T Q (P^T, dS^T over the consumed columns)
                         if (i == 1) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
-                        if (lane == 0) TRACE(3 * 1024 + (gc & 1023));
+                        if (lane == 0) TRACE_DKV(3 * 1024 + (gc & 1023));
                         mbar_wait(&bars->p_full[pb], ph_p);
                         tc_fence_after();
-                        if (lane == 0) TRACE(4 * 1024 + (gc & 1023));
+                        if (lane == 0) TRACE_DKV(4 * 1024 + (gc & 1023));
                         const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
                         const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
                         if (elect_one()) {
@@ -548,7 +553,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                             if (i == n) umma_commit(&bars->acc_full);
                         }
                         __syncwarp();
-                        if (lane == 0) TRACE(5 * 1024 + (gc & 1023));
+                        if (lane == 0) TRACE_DKV(5 * 1024 + (gc & 1023));
                         if (++st_a == STAGES) st_a = 0;
                         pb ^= 1;
                         if (pb == 0) ph_p ^= 1;
@@ -579,7 +584,7 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 const int qb = (k0 / BN + i) * BN;
                 const int32_t tcur = col_time(cx, qb, lane);
                 const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
-                mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
+                mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
                 float sv[32], dp[32];
                 tmem_ld32(tmem + lane_base + S_COL + sb * BN, sv);
@@ -610,9 +615,9 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
-                if (lane == 0 && (warp & 3) == 0) TRACE((6 + wg) * 1024 + (sc & 1023));
+                if (lane == 0 && (warp & 3) == 0) TRACE_DKV((6 + wg) * 1024 + (sc & 1023));
             }
-            mbar_wait(&bars->acc_full, ki & 1);
+            mbar_wait_sleep(&bars->acc_full, ki & 1);
             tc_fence_after();
             float dv[64], dk[64];
             tmem_ld32(tmem + lane_base + DV_COL + wg * 64, dv);

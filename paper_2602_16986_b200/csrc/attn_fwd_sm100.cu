@@ -71,6 +71,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     FwdBars* bars = reinterpret_cast<FwdBars*>(ts_s + 64);
 
     const int warp = threadIdx.x >> 5;
+    TRACE_SETUP();
     const int lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -97,7 +98,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const int q0 = it.tile * BM, h = it.head & 0xFFFF;
                 const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
                 const int n = key_tiles_count(kt);
-                mbar_wait(&bars->q_empty, (qi & 1) ^ 1);
+                mbar_wait_sleep(&bars->q_empty, (qi & 1) ^ 1);
                 mbar_arrive_expect_tx(&bars->q_full, QT);
                 tma_load_2d(sQ, &tmQ, &bars->q_full, h * DH, it.seq_start + q0);
                 tma_load_2d(sQ + QT / 2, &tmQ, &bars->q_full, h * DH + 64, it.seq_start + q0);
@@ -105,7 +106,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     const int row = it.seq_start + key_tile_at(kt, j) * BN;
                     const int s = kc % STAGES;
                     uint8_t* st = sKV + s * 2 * KT;
-                    mbar_wait(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
+                    mbar_wait_sleep(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
                     tma_load_2d(st, &tmK, &bars->kv_full[s], h * DH, row);
                     tma_load_2d(st + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
@@ -204,7 +205,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const int k0 = key_tile_at(kt, j) * BN;
                 const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
                 if (warp == 4 && lane == 0) TRACE(2 * 1024 + (sc & 1023));
-                mbar_wait(&bars->s_full[sb], (sc / NS) & 1);
+                mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
                 if (warp == 4 && lane == 0) TRACE(3 * 1024 + (sc & 1023));
                 tc_fence_after();
 #pragma unroll
@@ -239,7 +240,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (warp == 4 && lane == 0) TRACE(5 * 1024 + (sc & 1023));
             }
             // ---- O epilogue: A = O / N
-            mbar_wait(&bars->o_full, qi & 1);
+            mbar_wait_sleep(&bars->o_full, qi & 1);
             tc_fence_after();
             float ov[64];
             tmem_ld32(tmem + lane_base + O_COL + wg * 64, ov);

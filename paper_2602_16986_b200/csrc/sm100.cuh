@@ -48,6 +48,26 @@ UH_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint (ns): the thread sleeps until the phase completes or
+// the hint elapses, instead of re-polling and taking issue slots from co-resident warps.
+UH_DEV bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(addr), "r"(parity), "r"(1000000u) : "memory");
+    return ok != 0;
+}
+// Wait for a role whose wake-up latency is hidden (epilogue, producer): sleeping waiters
+// leave the SM sub-partition's issue slots to the warps that compute.  Traps after ~400 s.
+UH_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t n = 0;
+    while (!mbar_try_wait_sleep(addr, parity)) {
+        if (++n > 400000u) __trap();
+    }
+}
 // Blocking wait on the phase with the given parity.  A wait that never completes
 // traps after ~20 s of suspended retries (a deadlock becomes a launch error, not a hang).
 UH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
