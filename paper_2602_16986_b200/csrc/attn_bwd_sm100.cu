@@ -27,7 +27,7 @@ namespace uh {
 namespace {
 
 constexpr int DH = 128;
-constexpr int NUM_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 epilogue
+constexpr int NUM_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle (dkv: 2nd MMA), w4-11 epilogue
 
 __device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t row, int col, const float* v,
                                                 const void* gate, int64_t ldg, float scale) {
@@ -70,6 +70,7 @@ struct __align__(8) Bars {
     uint64_t kv_full[STAGES], kv_empty[STAGES];
     uint64_t s_full[NS], ds_full[NS];
     uint64_t dq_full, dq_empty;
+    ItemRing ring;
     uint32_t tmem;
 };
 
@@ -92,6 +93,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
         for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->ds_full[i], 8); }
         mbar_init(&bars->dq_full, 1); mbar_init(&bars->dq_empty, 8);
+        ring_init(&bars->ring, 9);   // MMA warp + 8 epilogue warps
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
@@ -107,7 +109,9 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         // ============================================================ producer
         if (lane == 0) {
             int kc = 0, qi = 0;
-            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+            for (;; ++qi) {
+                const int w = ring_claim_publish(&bars->ring, qi, a.counter, a.n_items);
+                if (w < 0) break;
                 const WorkItem it = a.items[w];
                 const int q0 = it.tile * BM, h = it.head & 0xFFFF;
                 const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
@@ -138,7 +142,9 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         constexpr uint32_t idesc_q = make_idesc_bf16(BM, DH, false, true);    // dS (TMEM) x K (MN-major)
         int kc = 0, sc = 0, qi = 0;
         const uint32_t q_addr = smem_u32(sQ), da_addr = smem_u32(sdA);
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+        for (;; ++qi) {
+            const int w = ring_take(&bars->ring, qi, lane);
+            if (w < 0) break;
             const WorkItem it = a.items[w];
             const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
             const int n = key_tiles_count(kt);
@@ -214,7 +220,9 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #pragma unroll
         for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
         int sc = 0, qi = 0;
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+        for (;; ++qi) {
+            const int w = ring_take(&bars->ring, qi, lane);
+            if (w < 0) break;
             const WorkItem it = a.items[w];
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int q0 = it.tile * BM;
@@ -403,19 +411,24 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 #define TRACE_DKV(x) do { } while (0)
 #endif
 namespace dkv {
-constexpr int BM = 128, BN = 32;          // 128 keys (MMA M), 32 queries per step
-constexpr int KT = BM * DH * 2;           // K / V staging tile (32 KB)
-constexpr int QT = BN * DH * 2;           // Q / dA tile (8 KB: 2 x 4 KB blocks of [32 rows x 128 B])
-constexpr int STAGES = 6;                 // (Q, dA) ring
+constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per step
+constexpr int KT = BM * DH * 2;           // K / V tile (32 KB: 2 x 16 KB blocks of [128 rows x 128 B])
+constexpr int QT = BN * DH * 2;           // Q / dA tile (16 KB: 2 x 8 KB blocks of [64 rows x 128 B])
+constexpr int KV_BUFS = 2;                // (K, V) double buffer: the next item's load overlaps this item
+constexpr int STAGES = 3;                 // (Q, dA) ring
 constexpr int NS = 2;                     // S^T / dP^T buffers
-constexpr int K_COL = 0, V_COL = 64, S_COL = 128, DP_COL = 192, DV_COL = 256, DK_COL = 384;
-constexpr int SMEM = 2 * KT + STAGES * 2 * QT + kPosTab * 4 + 256 + 1024 + 512;
+constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+constexpr int SMEM_DATA = KV_BUFS * 2 * KT + STAGES * 2 * QT + kPosTab * 4 + 256 + 512;
+constexpr int SMEM = 232448;              // the opt-in maximum: data plus as much alignment slack as remains
+static_assert(SMEM_DATA <= SMEM, "dkv shared memory");
 
 struct __align__(8) Bars {
-    uint64_t kv_full, kv_empty;
+    uint64_t kv_full[KV_BUFS], kv_empty[KV_BUFS];
     uint64_t qa_full[STAGES], qa_empty[STAGES];
     uint64_t s_full[NS], p_full[NS];
+    uint64_t issued[NS];          // dV/dK of the step in buffer b issued (orders the next S^T into b)
     uint64_t acc_full, acc_empty;
+    ItemRing ring;
     uint32_t tmem;
 };
 
@@ -424,14 +437,19 @@ __device__ __forceinline__ int n_qtiles(int k0, int L, int K1, int K2) {
     return (qe + BN - 1) / BN - k0 / BN;
 }
 
+// Per 128-key tile (K, V resident in shared memory for the whole item), over the 64-query
+// tiles that see it: S^T = K Q^T and dP^T = V dA^T (SS, N = 64) into TMEM; the epilogue
+// (warpgroup wg: queries [32 wg, 32 wg + 32)) writes P^T and dS^T (bf16) over the consumed
+// columns; dV += P^T dA and dK += dS^T Q read them as TMEM A operands.  64-query steps keep
+// the MMA issuer's per-step overhead (barrier waits, commits) well under the tensor time.
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem;
-    uint8_t* sV = smem + KT;
-    uint8_t* sQA = smem + 2 * KT;                 // [STAGES] x (Q 8 KB | dA 8 KB)
+    if (threadIdx.x == 0 && (smem - smem_raw) + SMEM_DATA > SMEM) __trap();   // alignment slack exhausted
+    uint8_t* sKV = smem;                          // [KV_BUFS] x (K 32 KB | V 32 KB)
+    uint8_t* sQA = smem + KV_BUFS * 2 * KT;       // [STAGES] x (Q 16 KB | dA 16 KB)
     float* pos_s = reinterpret_cast<float*>(sQA + STAGES * 2 * QT);
     float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
@@ -439,10 +457,13 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     TRACE_SETUP();
 
     if (threadIdx.x == 0) {
-        mbar_init(&bars->kv_full, 1); mbar_init(&bars->kv_empty, 1);
+        for (int i = 0; i < KV_BUFS; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->qa_full[i], 1); mbar_init(&bars->qa_empty[i], 1); }
-        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 4); }
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 8); mbar_init(&bars->issued[i], 1);
+        }
         mbar_init(&bars->acc_full, 1); mbar_init(&bars->acc_empty, 8);
+        ring_init(&bars->ring, 10);  // MMA warps 1, 3 + 8 epilogue warps
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
@@ -456,16 +477,20 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         // ============================================================ producer
         if (lane == 0) {
             int qc = 0, ki = 0;
-            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+            for (;; ++ki) {
+                const int w = ring_claim_publish(&bars->ring, ki, a.counter, a.n_items);
+                if (w < 0) break;
                 const WorkItem it = a.items[w];
                 const int k0 = it.tile * BM, h = it.head & 0xFFFF;
                 const int n = n_qtiles(k0, it.seq_len, a.K1, a.K2);
-                mbar_wait_sleep(&bars->kv_empty, (ki & 1) ^ 1);
-                mbar_arrive_expect_tx(&bars->kv_full, 2 * KT);
-                tma_load_2d(sK, &tmK, &bars->kv_full, h * DH, it.seq_start + k0);
-                tma_load_2d(sK + KT / 2, &tmK, &bars->kv_full, h * DH + 64, it.seq_start + k0);
-                tma_load_2d(sV, &tmV, &bars->kv_full, h * DH, it.seq_start + k0);
-                tma_load_2d(sV + KT / 2, &tmV, &bars->kv_full, h * DH + 64, it.seq_start + k0);
+                const int kb = ki & 1;
+                uint8_t* sK = sKV + kb * 2 * KT;
+                mbar_wait_sleep(&bars->kv_empty[kb], ((ki >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bars->kv_full[kb], 2 * KT);
+                tma_load_2d(sK, &tmK, &bars->kv_full[kb], h * DH, it.seq_start + k0);
+                tma_load_2d(sK + KT / 2, &tmK, &bars->kv_full[kb], h * DH + 64, it.seq_start + k0);
+                tma_load_2d(sK + KT, &tmV, &bars->kv_full[kb], h * DH, it.seq_start + k0);
+                tma_load_2d(sK + KT + KT / 2, &tmV, &bars->kv_full[kb], h * DH + 64, it.seq_start + k0);
                 for (int i = 0; i < n; ++i) {
                     const int row = it.seq_start + (k0 / BN + i) * BN;
                     const int s = qc % STAGES;
@@ -480,85 +505,88 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 }
             }
         }
-    } else if (warp == 1) {
-        // ============================================================ MMA issuer
-        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [K|V](TMEM) x [Q|dA]^T
+    } else if (warp == 1 || warp == 3) {
+        // ============================================================ MMA issuers
+        // Two warps feed the one tensor pipe: warp 1 issues S^T / dP^T, warp 3 issues dV / dK, so
+        // one warp's barrier wait (~130 cycles even when complete) overlaps the other's issue and
+        // the 4-5 deep MMA queue does not drain.  S^T(i + 2) reuses the TMEM buffer that
+        // dV/dK(i) reads: warp 1 waits for "issued" (fence::before/after_thread_sync around it
+        // order the two warps' tcgen05.mma in the pipe).  Each warp runs convergently
+        // (descriptors in uniform registers); one elected lane issues each block.
+        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [K|V] x [Q|dA]^T (both K-major)
         constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // [P^T|dS^T](TMEM) x [dA|Q] (MN-major)
-        // The whole warp runs the role convergently (so descriptors live in uniform registers);
-        // one elected lane issues each step's tcgen05.mma block back to back from precomputed
-        // descriptors: at 32 queries per step the issue stream, not the tensor pipe, is the limit.
-        {
-            const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV);
-            const uint64_t q_k = make_sw128_desc(smem_u32(sQA), 16, 1024);        // Q / dA K-major (S^T, dP^T)
-            const uint64_t q_mn = make_sw128_desc(smem_u32(sQA), QT / 2, 1024);   // Q / dA MN-major (dK, dV)
-            int st_s = 0, ph_s = 0;       // (Q, dA) stage consumed by S^T / dP^T
-            int st_a = 0;                 // stage consumed by dV / dK (trails st_s)
-            int sb = 0, ph_p = 0;         // S buffer of the next S^T; p_full parity of buffer pb
-            int pb = 0;
-            int ki = 0, sc = 0, gc = 0;
-            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+        int ki = 0, sc = 0;
+        if (warp == 1) {
+            const uint64_t kv_k = make_sw128_desc(smem_u32(sKV), 16, 1024);      // K / V K-major (A)
+            const uint64_t q_k = make_sw128_desc(smem_u32(sQA), 16, 1024);       // Q / dA K-major (B)
+            int st_s = 0, ph_s = 0;
+            for (;; ++ki) {
+                const int w = ring_take(&bars->ring, ki, lane);
+                if (w < 0) break;
                 const WorkItem it = a.items[w];
                 const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
-                mbar_wait(&bars->kv_full, ki & 1);
-                tc_fence_after();
-                if (elect_one()) {
+                const int kb = ki & 1;
+                const uint64_t dk = kv_k + ((uint32_t)(kb * 2 * KT) >> 4), dv = dk + (KT >> 4);
+                mbar_wait(&bars->kv_full[kb], (ki >> 1) & 1);
+                for (int i = 0; i < n; ++i, ++sc) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
+                    const int sb = sc & 1;
+                    if (lane == 0) TRACE_DKV(0 * 1024 + (sc & 1023));
+                    mbar_wait(&bars->qa_full[st_s], ph_s);
+                    if (sc >= NS) mbar_wait(&bars->issued[sb], ((sc >> 1) - 1) & 1);
+                    tc_fence_after();
+                    if (lane == 0) TRACE_DKV(1 * 1024 + (sc & 1023));
+                    const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
+                    const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < DH / 16; ++kk) {   // K, V: smem -> TMEM (A operands of S^T, dP^T)
-                        const uint32_t off = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
-                        tmem_cp_128x256b(tmem + K_COL + kk * 8, make_sw128_desc(k_addr + off, 16, 1024));
-                        tmem_cp_128x256b(tmem + V_COL + kk * 8, make_sw128_desc(v_addr + off, 16, 1024));
+                        for (int kk = 0; kk < DH / 16; ++kk) {
+                            const uint32_t oa = ((kk >> 2) * (KT / 2) + (kk & 3) * 32) >> 4;
+                            const uint32_t ob = ((kk >> 2) * (QT / 2) + (kk & 3) * 32) >> 4;
+                            umma_ss(d_s, dk + oa, dq + ob, idesc_s, kk > 0 ? 1u : 0u);
+                            umma_ss(d_p, dv + oa, dda + ob, idesc_s, kk > 0 ? 1u : 0u);
+                        }
+                        umma_commit(&bars->s_full[sb]);
+                        if (i == n - 1) umma_commit(&bars->kv_empty[kb]);   // K, V read by the last S^T / dP^T
                     }
-                    umma_commit(&bars->kv_empty);
+                    __syncwarp();
+                    if (lane == 0) TRACE_DKV(2 * 1024 + (sc & 1023));
+                    if (++st_s == STAGES) { st_s = 0; ph_s ^= 1; }
                 }
-                __syncwarp();
-                for (int i = 0; i <= n; ++i) {
-                    if (i < n) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
-                        if (lane == 0) TRACE_DKV(0 * 1024 + (sc & 1023));
-                        mbar_wait(&bars->qa_full[st_s], ph_s);
-                        tc_fence_after();
-                        if (lane == 0) TRACE_DKV(1 * 1024 + (sc & 1023));
-                        const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
-                        const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
-                        if (elect_one()) {
+            }
+        } else {
+            const uint64_t q_mn = make_sw128_desc(smem_u32(sQA), QT / 2, 1024);  // Q / dA MN-major (B)
+            int st_a = 0;
+            for (;; ++ki) {
+                const int w = ring_take(&bars->ring, ki, lane);
+                if (w < 0) break;
+                const WorkItem it = a.items[w];
+                const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+                for (int i = 0; i < n; ++i, ++sc) {   // ---- dV += P^T dA, dK += dS^T Q
+                    const int pb = sc & 1;
+                    if (i == 0) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
+                    if (lane == 0) TRACE_DKV(3 * 1024 + (sc & 1023));
+                    mbar_wait(&bars->p_full[pb], (sc >> 1) & 1);
+                    tc_fence_after();
+                    if (lane == 0) TRACE_DKV(4 * 1024 + (sc & 1023));
+                    const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
+                    const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
+                    if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < DH / 16; ++kk) {
-                                const uint32_t ob = ((kk >> 2) * (QT / 2) + (kk & 3) * 32) >> 4;
-                                umma_ts(d_s, tmem + K_COL + kk * 8, dq + ob, idesc_s, kk > 0 ? 1u : 0u);
-                                umma_ts(d_p, tmem + V_COL + kk * 8, dda + ob, idesc_s, kk > 0 ? 1u : 0u);
-                            }
-                            umma_commit(&bars->s_full[sb]);
+                        for (int kk = 0; kk < BN / 16; ++kk) {
+                            // queries [16 kk, 16 kk + 16): packed by warpgroup kk / 2 at column 32 (kk / 2) + 8 (kk % 2)
+                            const uint32_t ca = (kk >> 1) * 32 + (kk & 1) * 8;
+                            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                            umma_ts(tmem + DV_COL, a_p + ca, dda + kk * (2048 >> 4), idesc_a, acc);
+                            umma_ts(tmem + DK_COL, a_d + ca, dq + kk * (2048 >> 4), idesc_a, acc);
                         }
-                        __syncwarp();
-                        if (lane == 0) TRACE_DKV(2 * 1024 + (sc & 1023));
-                        if (++st_s == STAGES) { st_s = 0; ph_s ^= 1; }
-                        sb ^= 1;
-                        ++sc;
+                        umma_commit(&bars->qa_empty[st_a]);
+                        if (i == n - 1) umma_commit(&bars->acc_full);
                     }
-                    if (i >= 1) {  // ---- dV += P^T dA, dK += dS^T Q (P^T, dS^T over the consumed columns)
-                        if (i == 1) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
-                        if (lane == 0) TRACE_DKV(3 * 1024 + (gc & 1023));
-                        mbar_wait(&bars->p_full[pb], ph_p);
-                        tc_fence_after();
-                        if (lane == 0) TRACE_DKV(4 * 1024 + (gc & 1023));
-                        const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
-                        const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
-                        if (elect_one()) {
-#pragma unroll
-                            for (int kk = 0; kk < BN / 16; ++kk) {
-                                const uint32_t acc = (i > 1 || kk > 0) ? 1u : 0u;
-                                umma_ts(tmem + DV_COL, a_p + kk * 8, dda + kk * (2048 >> 4), idesc_a, acc);
-                                umma_ts(tmem + DK_COL, a_d + kk * 8, dq + kk * (2048 >> 4), idesc_a, acc);
-                            }
-                            umma_commit(&bars->qa_empty[st_a]);
-                            if (i == n) umma_commit(&bars->acc_full);
-                        }
-                        __syncwarp();
-                        if (lane == 0) TRACE_DKV(5 * 1024 + (gc & 1023));
-                        if (++st_a == STAGES) st_a = 0;
-                        pb ^= 1;
-                        if (pb == 0) ph_p ^= 1;
-                        ++gc;
-                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->issued[pb]);
+                    if (lane == 0) TRACE_DKV(5 * 1024 + (sc & 1023));
+                    if (++st_a == STAGES) st_a = 0;
                 }
             }
         }
@@ -569,7 +597,9 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const float ha = 0.5f * a.alpha;
         int sc = 0, ki = 0;
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++ki) {
+        for (;; ++ki) {
+            const int w = ring_take(&bars->ring, ki, lane);
+            if (w < 0) break;
             const WorkItem it = a.items[w];
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int k0 = it.tile * BM;
@@ -579,16 +609,19 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
             const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
             for (int i = 0; i < n; ++i, ++sc) {
-                if ((sc & 1) != wg) continue;       // q tiles alternate between the warpgroups
                 const int sb = sc % NS;
-                const int qb = (k0 / BN + i) * BN;
+                const int qb = (k0 / BN + i) * BN + 32 * wg;   // this warpgroup's 32 queries
                 const int32_t tcur = col_time(cx, qb, lane);
                 const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
                 mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
                 tc_fence_after();
+#if UH_EXP == 1
+                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+                continue;
+#endif
                 float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + S_COL + sb * BN, sv);
-                tmem_ld32(tmem + lane_base + DP_COL + sb * BN, dp);
+                tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * wg, sv);
+                tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * wg, dp);
                 tmem_ld_wait();
                 // p' = silu(2h) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  t = tanh(h); bf16x2
                 float hx[32];
@@ -609,8 +642,8 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         if (!k_visible(cx, kp, kok, qb + c)) { zero_half(p2, c); zero_half(d2, c); }
                 }
                 // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
-                tmem_st16(tmem + lane_base + S_COL + sb * BN, p2);
-                tmem_st16(tmem + lane_base + DP_COL + sb * BN, d2);
+                tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);
+                tmem_st16(tmem + lane_base + DP_COL + sb * BN + 32 * wg, d2);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -656,7 +689,7 @@ uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStr
     note_launch();
     UH_CUDA(cudaGetLastError());
 
-    CUtensorMap q32, dA32, k128, v128;
+    CUtensorMap q32, dA32, k128, v128;   // q / dA boxes of dkv::BN rows
     UH_TRY(make_tmap_bf16(&q32, akv.q, width, T, akv.ld_qkv, 64, dkv::BN));
     UH_TRY(make_tmap_bf16(&dA32, akv.dout, width, T, akv.ld_dout, 64, dkv::BN));
     UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));

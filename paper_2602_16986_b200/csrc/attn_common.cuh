@@ -51,6 +51,19 @@ struct AttnArgs {
     int* counter;                          // dynamic work counter (persistent kernels)
 };
 
+// Dynamic work distribution for the persistent tcgen05 kernels: the producer lane claims
+// the next item of the cost-descending list (F0) with one atomicAdd, so the list is served
+// longest-first to whichever CTA frees up (LPT), and publishes it to the CTA's other roles
+// through a small shared-memory ring (mbarrier full/empty per slot).  -1 ends the stream.
+constexpr int kItemRing = 4;
+struct ItemRing {
+    uint64_t full[kItemRing], empty[kItemRing];
+    int idx[kItemRing];
+};
+UH_DEV void ring_init(ItemRing* r, int consumer_warps);
+UH_DEV int ring_claim_publish(ItemRing* r, int k, int* counter, int n_items);
+UH_DEV int ring_take(ItemRing* r, int k, int lane);
+
 UH_HD bool mask_ok(int q, int k, int K1, int K2) {
     return k <= q && (q - k <= K1 || k < K2);
 }
@@ -355,6 +368,29 @@ UH_DEV ChunkCtx make_ctx(const AttnArgs& a, const float* pos_e, const float* ts_
     c.K1 = a.K1; c.K2 = a.K2; c.L = L;
     c.ha = 0.5f * a.alpha;
     return c;
+}
+
+
+UH_DEV void ring_init(ItemRing* r, int consumer_warps) {
+    for (int i = 0; i < kItemRing; ++i) { mbar_init(&r->full[i], 1); mbar_init(&r->empty[i], consumer_warps); }
+}
+// producer lane: claim, publish (the slot is free once every consumer warp has read it)
+UH_DEV int ring_claim_publish(ItemRing* r, int k, int* counter, int n_items) {
+    const int s = k % kItemRing;
+    mbar_wait_sleep(&r->empty[s], ((k / kItemRing) & 1) ^ 1);
+    const int w = atomicAdd(counter, 1);
+    r->idx[s] = w < n_items ? w : -1;
+    mbar_arrive(&r->full[s]);   // release: the index is visible to the waiting roles
+    return w < n_items ? w : -1;
+}
+// whole warp: the k-th item of this CTA (or -1)
+UH_DEV int ring_take(ItemRing* r, int k, int lane) {
+    const int s = k % kItemRing;
+    mbar_wait_sleep(&r->full[s], (k / kItemRing) & 1);
+    const int w = *reinterpret_cast<volatile int*>(&r->idx[s]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&r->empty[s]);
+    return w;
 }
 
 }  // namespace uh

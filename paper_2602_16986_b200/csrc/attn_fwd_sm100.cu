@@ -45,6 +45,7 @@ struct __align__(8) FwdBars {
     uint64_t s_full[NS];
     uint64_t p_full[NS];
     uint64_t o_full, o_empty;
+    ItemRing ring;
     uint32_t tmem;
 };
 
@@ -79,6 +80,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
         for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 4); }
         mbar_init(&bars->o_full, 1); mbar_init(&bars->o_empty, 8);
+        ring_init(&bars->ring, 9);   // MMA warp + 8 epilogue warps
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
@@ -93,7 +95,9 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         // ============================================================ producer
         if (lane == 0) {
             int kc = 0, qi = 0;
-            for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+            for (;; ++qi) {
+                const int w = ring_claim_publish(&bars->ring, qi, a.counter, a.n_items);
+                if (w < 0) break;
                 const WorkItem it = a.items[w];
                 const int q0 = it.tile * BM, h = it.head & 0xFFFF;
                 const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
@@ -122,7 +126,9 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         constexpr uint32_t idesc_o = make_idesc_bf16(BM, DH, false, true);   // P (K-major) x V (MN-major)
         int kc = 0, sc = 0, pc = 0, qi = 0;
         const uint32_t q_addr = smem_u32(sQ);
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+        for (;; ++qi) {
+            const int w = ring_take(&bars->ring, qi, lane);
+            if (w < 0) break;
             const WorkItem it = a.items[w];
             const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
             const int n = key_tiles_count(kt);
@@ -187,7 +193,9 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const float ha = 0.5f * a.alpha;
         int sc = 0, qi = 0;
-        for (int w = blockIdx.x; w < a.n_items; w += gridDim.x, ++qi) {
+        for (;; ++qi) {
+            const int w = ring_take(&bars->ring, qi, lane);
+            if (w < 0) break;
             const WorkItem it = a.items[w];
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int q0 = it.tile * BM;
