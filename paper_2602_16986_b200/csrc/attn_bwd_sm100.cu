@@ -60,10 +60,11 @@ namespace dq {
 constexpr int BM = 128, BN = 64;
 constexpr int QT = BM * DH * 2;         // Q / dA tile bytes (2 x 16 KB swizzled blocks)
 constexpr int KT = BN * DH * 2;         // K / V tile bytes (2 x 8 KB blocks)
-constexpr int STAGES = 4;               // (K, V) ring
+constexpr int STAGES = 3;               // (K, V) ring
 constexpr int NS = 2;                   // S / dP buffers in TMEM
 constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256, Q_COL = 384, DA_COL = 448;
-constexpr int SMEM = 2 * QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512 + 1024;
+constexpr int TSL = 8 * 32 * 32 * 4;   // d time_bias partials [8 warps][32 buckets][32 lanes]
+constexpr int SMEM = 2 * QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512 + TSL;
 
 struct __align__(8) Bars {
     uint64_t qa_full, qa_empty;
@@ -97,8 +98,8 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         fence_barrier_init();
     }
     stage_rab(a, pos_s, ts_s);
-    float* tsw = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);   // [8 warps][32] d time_bias
-    if (threadIdx.x < 256) tsw[threadIdx.x] = 0.f;
+    float* tsl = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);   // [8 warps][32 buckets][32 lanes]
+    for (int i = threadIdx.x; i < TSL / 4; i += NUM_THREADS) tsl[i] = 0.f;
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
@@ -233,51 +234,37 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
             // d rab partials of one 32-column chunk; runs after ds_full (off the S -> dS -> next-S
-            // chain, overlapping the tensor pipe).  d time_bias: lanes grouped by bucket, a warp
-            // sum, one lane adds into this warp's shared row (no atomics, no local memory).
-            float* const tsw_w = tsw + (warp - 4) * 32;
-            auto bucket_add = [&](int bb, float v) {   // bb per lane (-1: none)
-                unsigned pend = __ballot_sync(0xffffffffu, bb >= 0);
-                while (pend) {
-                    const int lb = __shfl_sync(0xffffffffu, bb, __ffs(pend) - 1);
-                    const bool mine = bb == lb;
-                    float x = mine ? v : 0.f;
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-                    if (lane == 0) tsw_w[lb] += x;
-                    pend &= ~__ballot_sync(0xffffffffu, mine);
-                }
-            };
+            // chain, overlapping the tensor pipe).  d time_bias goes to this lane's own column of
+            // a shared [bucket][lane] table (conflict-free, no atomics, no local memory).
+            float* const tsl_l = tsl + (warp - 4) * 1024 + lane;
             auto rab_grads = [&](const Chunk& ch, const uint32_t* d2, int kb) {
                 const float tsum = sum_packed16(d2);   // rows beyond L carry zeros
                 if (a.dts) {
                     if (!(ch.flags & FLAG_T2)) {
                         float so = 0.f;                // columns [0, n) are in bucket b_other (FLAG_T1)
-                        if (ch.flags & FLAG_T1) {
+                        if ((ch.flags & FLAG_T1) && ch.n > 0) {
                             uint32_t m2[16];
 #pragma unroll
                             for (int i = 0; i < 16; ++i)
                                 m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
                             so = sum_packed16(m2);
-                            bucket_add(qok && ch.n > 0 ? ch.b_other : -1, so);
+                            if (qok) tsl_l[ch.b_other * 32] += so;
                         }
-                        bucket_add(qok ? ch.b_base : -1, tsum - so);
-                    } else {                           // next to the diagonal: per-element buckets
-                        int bk[32];
+                        if (qok) tsl_l[ch.b_base * 32] += tsum - so;
+                    } else {                           // next to the diagonal: per-element buckets,
+                        int bk[32];                    // monotone along the row (runs flushed on change)
 #pragma unroll
                         for (int c = 0; c < 32; ++c) bk[c] = bucket32(tq - __shfl_sync(0xffffffffu, ch.tcol, c), cx.NB);
-                        const int lo = __reduce_min_sync(0xffffffffu, qok ? ch.b_base : 64);
-                        const int hi = __reduce_max_sync(0xffffffffu, qok ? ch.b_other : -1);
-                        for (int bb = lo; bb <= hi; ++bb) {   // warp-uniform
-                            float x = 0.f;
+                        if (qok) {
+                            int cur = bk[0];
+                            float acc = 0.f;
 #pragma unroll
                             for (int c = 0; c < 32; ++c) {
                                 const float2 u = unpack_bf16x2(d2[c >> 1]);
-                                x += bk[c] == bb ? ((c & 1) ? u.y : u.x) : 0.f;
+                                if (bk[c] != cur) { tsl_l[cur * 32] += acc; cur = bk[c]; acc = 0.f; }
+                                acc += (c & 1) ? u.y : u.x;
                             }
-#pragma unroll
-                            for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-                            if (lane == 0) tsw_w[bb] += x;
+                            tsl_l[cur * 32] += acc;
                         }
                     }
                 }
@@ -325,6 +312,7 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     // ds' = dP (1 + t)(1 + h (1 - t)), h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
                     float hx[32];
                     q_h<false>(cx, ch, tq, sv, hx, nullptr);
+                    if (ch.flags & FLAG_M) apply_vis(dp, q_vis_bits(cx, qp, qok, kb));   // dP = 0 -> dS = 0
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
@@ -333,11 +321,6 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                         const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
                         d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
                     }
-                }
-                if (ch.flags & FLAG_M) {
-#pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (!q_visible(cx, qp, qok, kb + c)) zero_half(d2, c);
                 }
                 if (!qok) {
 #pragma unroll
@@ -377,11 +360,15 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
             if (lane == 0) redp[kMaxNearT * 32 * 8 + ew] = f;
             named_bar_sync(2, 256);
-            if (a.dts && et < a.NB) {
+            if (a.dts) {                       // bucket et >> 3, warp et & 7: 32 lanes, then 8 warps
+                const int b = et >> 3, w8 = et & 7;
                 float sum = 0.f;
-#pragma unroll
-                for (int w8 = 0; w8 < 8; ++w8) sum += tsw[w8 * 32 + et];
-                if (sum != 0.f) atomicAdd(a.dts + et, sum * rscale);
+#pragma unroll 8
+                for (int l = 0; l < 32; ++l) sum += tsl[(w8 * 32 + b) * 32 + l];
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+                if (w8 == 0 && b < a.NB && sum != 0.f) atomicAdd(a.dts + b, sum * rscale);
             }
             if (a.dpos) {
                 if (et < a.P - 1) {
@@ -626,6 +613,11 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 // p' = silu(2h) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  t = tanh(h); bf16x2
                 float hx[32];
                 k_h(cx, ch, tk, sv, hx);
+                if (ch.flags & FLAG_M) {          // h = 0 and dP = 0 -> P = dS = 0
+                    const uint32_t m = k_vis_bits(cx, kp, kok, qb);
+                    apply_vis(hx, m);
+                    apply_vis(dp, m);
+                }
                 uint32_t p2[16], d2[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
@@ -635,11 +627,6 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     p2[c] = mul_bf16x2(h2, a1);
                     const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
                     d2[c] = mul_bf16x2(pack_bf16(dp[2 * c], dp[2 * c + 1]), mul_bf16x2(a1, wv));
-                }
-                if (ch.flags & FLAG_M) {
-#pragma unroll
-                    for (int c = 0; c < 32; ++c)
-                        if (!k_visible(cx, kp, kok, qb + c)) { zero_half(p2, c); zero_half(d2, c); }
                 }
                 // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
                 tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);

@@ -310,6 +310,37 @@ UH_DEV void k_h(const ChunkCtx& c, const Chunk& ch, int32_t tk, const float* s, 
     }
 }
 
+// Visibility of a 32-column chunk as a bit mask (bit c = column c visible), for FLAG_M
+// chunks: causal, window and global-prefix bounds are column ranges, so the mask costs a
+// few integer ops per chunk instead of a predicate per element.
+UH_DEV uint32_t bit_range(int lo, int hi) {   // bits [lo, hi] of 0..31 (empty if hi < lo)
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > 31 ? 31 : hi;
+    if (hi < lo) return 0u;
+    const uint32_t up = hi == 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u);
+    return up & ~((1u << lo) - 1u);
+}
+constexpr int kHugeWindow = 0x40000000;   // K1 at or beyond this is "full causal"
+// query row qp, key columns kb..kb+31 (k <= q < L, so the length bound is implied)
+UH_DEV uint32_t q_vis_bits(const ChunkCtx& c, int qp, bool qok, int kb) {
+    if (!qok) return 0u;
+    const int d = qp - kb;                                            // column of k == q
+    const uint32_t win = c.K1 >= kHugeWindow ? 0xFFFFFFFFu : bit_range(d - c.K1, 31);
+    return bit_range(0, d) & (win | bit_range(0, c.K2 - kb - 1));
+}
+// key row kp, query columns qb..qb+31
+UH_DEV uint32_t k_vis_bits(const ChunkCtx& c, int kp, bool kok, int qb) {
+    if (!kok) return 0u;
+    const int d = kp - qb;                                            // column of q == k
+    const uint32_t win = (kp < c.K2 || c.K1 >= kHugeWindow) ? 0xFFFFFFFFu : bit_range(0, d + c.K1);
+    return bit_range(d, 31) & win & bit_range(0, c.L - qb - 1);
+}
+// zero the fp32 values of invisible columns (before they are packed to bf16)
+UH_DEV void apply_vis(float* v, uint32_t m) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (m >> j) & 1u ? v[j] : 0.f;
+}
+
 // per-element visibility (only needed when FLAG_M)
 UH_DEV bool q_visible(const ChunkCtx& c, int qp, bool qok, int kp) {
     return qok && kp < c.L && mask_ok(qp, kp, c.K1, c.K2);

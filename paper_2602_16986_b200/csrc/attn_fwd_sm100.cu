@@ -226,16 +226,12 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     // h = (alpha S + rab)/2 in fp32, then packed bf16x2: silu(2h) = h + h tanh(h)
                     float hx[32];
                     q_h<false>(cx, ch, tq, s, hx, nullptr);
+                    if (ch.flags & FLAG_M) apply_vis(hx, q_vis_bits(cx, qp, qok, kb));   // h = 0 -> P = 0
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
                         pk[i] = fma_bf16x2(h2, tanh_bf16x2(h2), h2);
-                    }
-                    if (ch.flags & FLAG_M) {
-#pragma unroll
-                        for (int c = 0; c < 32; ++c)
-                            if (!q_visible(cx, qp, qok, kb + c)) zero_half(pk, c);
                     }
                     // P -> TMEM over the chunk's own (already read) S columns: keys [32hc, 32hc+32) at col 32hc
                     tmem_st16(tmem + lane_base + sb * BN + 32 * hc, pk);
