@@ -110,6 +110,12 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     else      UH_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
     if (!BMN) UH_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
     else      UH_TRY(make_tmap_bf16(&tb, g.B, g.N, g.K, g.ldb, 64, 64));
+    // outputs leave through TMA stores of 32x32 boxes (64B swizzle, matching the staging layout)
+    CUtensorMap to0 = ta, to1 = ta;
+    if (EPI != EPI_F32) {
+        UH_TRY(make_tmap_bf16(&to0, g.out0, g.N, g.M, g.ld0, 32, 32, 64));
+        if (g.out1) UH_TRY(make_tmap_bf16(&to1, g.out1, g.N, g.M, g.ld1, 32, 32, 64));
+    }
     GemmArgs a;
     a.M = g.M; a.N = g.N; a.K = g.K;
     a.m_tiles = (g.M + C::BM - 1) / C::BM;
@@ -128,7 +134,7 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     const int total = a.m_tiles * a.n_tiles * a.k_splits;
     auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI>;
     UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    kern<<<std::min(total, sms), 384, C::SMEM, st>>>(ta, tb, a);
+    kern<<<std::min(total, sms), 384, C::SMEM, st>>>(ta, tb, to0, to1, a);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;

@@ -40,19 +40,22 @@ struct GemmCfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int STAGING = 8 * 2 * 2048;   // per epilogue warp: a 32x32 bf16 box per output
+    static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
 };
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(384, 1)
-gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1, GemmArgs g) {
     using C = GemmCfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES;   // epilogue staging for the TMA stores
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::STAGING);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;   // [2]
     uint64_t* tempty = tfull + 2;          // [2]
@@ -171,19 +174,33 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + c0, v);
                 tmem_ld_wait();
                 const int col = nt * BN + c0;
-                if (!row_ok || col >= g.N) continue;
+                if (col >= g.N) continue;   // warp-uniform
                 if (EPI == EPI_F32) {
+                    if (!row_ok) continue;
                     float* o = reinterpret_cast<float*>(g.out0) + (int64_t)row * g.ld0 + col;
 #pragma unroll
                     for (int j = 0; j < 32; j += 4)
                         atomicAdd(reinterpret_cast<float4*>(o + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
                 } else {
-                    if (g.bias) {
+                    // h = acc + bias (EPI_SILU: h/2 carried, silu(2h') = h' + h' tanh h'); packed bf16
+                    float hb[32];
+                    const float bsc = EPI == EPI_SILU ? 0.5f : 1.0f;
+                    if (g.bias && col + 32 <= g.N) {
+                        const float4* bp = reinterpret_cast<const float4*>(g.bias + col);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] += __ldg(g.bias + col + j);
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 b4 = __ldg(bp + j);
+                            hb[4 * j] = b4.x * bsc; hb[4 * j + 1] = b4.y * bsc; hb[4 * j + 2] = b4.z * bsc; hb[4 * j + 3] = b4.w * bsc;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) hb[j] = (g.bias && col + j < g.N) ? __ldg(g.bias + col + j) * bsc : 0.f;
                     }
+                    uint32_t o0[16], o1[16];
                     if (EPI == EPI_BF16) {
-                        if (g.resid) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] += hb[j];
+                        if (g.resid && row_ok) {
                             const uint4* rp = reinterpret_cast<const uint4*>(g.resid + (int64_t)row * g.ldr + col);
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
@@ -197,33 +214,40 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                 }
                             }
                         }
-                        uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out0) + (int64_t)row * g.ld0 + col);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            op[j] = make_uint4(pack_bf16(v[j * 8 + 0], v[j * 8 + 1]), pack_bf16(v[j * 8 + 2], v[j * 8 + 3]),
-                                               pack_bf16(v[j * 8 + 4], v[j * 8 + 5]), pack_bf16(v[j * 8 + 6], v[j * 8 + 7]));
-                    } else {  // EPI_SILU
-                        // silu(v) = h (1 + t), silu'(v) = (1 + t)(1 + h (1 - t)) / 2, h = v/2, t = tanh(h)
-                        float s[32], gp[32];
+                        for (int i = 0; i < 16; ++i) o0[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                    } else {  // EPI_SILU (fp32): silu = h + h t;  silu' = (1 + t)(1 + h (1 - t)) / 2;  h = acc/2, t = tanh h
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float hv = 0.5f * v[j];
-                            const float t = tanh_approx(hv);
-                            s[j] = fmaf(hv, t, hv);
-                            gp[j] = 0.5f * (1.0f + t) * fmaf(hv, 1.0f - t, 1.0f);
+                        for (int i = 0; i < 16; ++i) {
+                            const float h0 = fmaf(v[2 * i], 0.5f, hb[2 * i]), h1 = fmaf(v[2 * i + 1], 0.5f, hb[2 * i + 1]);
+                            const float t0 = tanh_approx(h0), t1 = tanh_approx(h1);
+                            o0[i] = pack_bf16(fmaf(h0, t0, h0), fmaf(h1, t1, h1));
+                            if (g.out1)
+                                o1[i] = pack_bf16(fmaf(t0, 0.5f, 0.5f) * (fmaf(-h0, t0, h0) + 1.f),
+                                                  fmaf(t1, 0.5f, 0.5f) * (fmaf(-h1, t1, h1) + 1.f));
                         }
-                        uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out0) + (int64_t)row * g.ld0 + col);
+                    }
+                    // rows of this warp -> its 64B-swizzled 32x32 staging boxes -> TMA stores
+                    // (coalesced; rows / columns beyond M, N are clipped by the tensor map)
+                    uint8_t* box0 = stg + (warp - 4) * 4096;
+                    uint8_t* box1 = box0 + 2048;
+                    if (lane_id() == 0) bulk_wait_read0();   // the previous stores have read the boxes
+                    __syncwarp();
+                    const int r = lane_id();
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            op[j] = make_uint4(pack_bf16(s[j * 8 + 0], s[j * 8 + 1]), pack_bf16(s[j * 8 + 2], s[j * 8 + 3]),
-                                               pack_bf16(s[j * 8 + 4], s[j * 8 + 5]), pack_bf16(s[j * 8 + 6], s[j * 8 + 7]));
-                        if (g.out1) {
-                            uint4* gq = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(g.out1) + (int64_t)row * g.ld1 + col);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                gq[j] = make_uint4(pack_bf16(gp[j * 8 + 0], gp[j * 8 + 1]), pack_bf16(gp[j * 8 + 2], gp[j * 8 + 3]),
-                                                   pack_bf16(gp[j * 8 + 4], gp[j * 8 + 5]), pack_bf16(gp[j * 8 + 6], gp[j * 8 + 7]));
-                        }
+                    for (int c = 0; c < 4; ++c) {
+                        const int off = r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+                        *reinterpret_cast<uint4*>(box0 + off) = make_uint4(o0[4 * c], o0[4 * c + 1], o0[4 * c + 2], o0[4 * c + 3]);
+                        if (EPI == EPI_SILU && g.out1)
+                            *reinterpret_cast<uint4*>(box1 + off) = make_uint4(o1[4 * c], o1[4 * c + 1], o1[4 * c + 2], o1[4 * c + 3]);
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane_id() == 0) {
+                        const int row0 = mt * C::BM + wq * 32;
+                        tma_store_2d(&tmO0, box0, col, row0);
+                        if (EPI == EPI_SILU && g.out1) tma_store_2d(&tmO1, box1, col, row0);
+                        bulk_commit();
                     }
                 }
             }
@@ -232,6 +256,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             if (lane_id() == 0) mbar_arrive(&tempty[acc]);
         }
     }
+    if (warp >= 4 && lane_id() == 0) bulk_wait0();   // TMA stores complete before the CTA retires
     __syncthreads();
     if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }

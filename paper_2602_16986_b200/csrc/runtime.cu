@@ -40,7 +40,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                         uint32_t box_inner, uint32_t box_outer) {
+                         uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
     auto enc = get_encode();
     if (!enc) return fail(UH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     if (outer == 0) outer = 1;  // empty tensors are never read; keep the descriptor valid
@@ -49,7 +49,9 @@ uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(UH_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
