@@ -39,10 +39,12 @@ __global__ void __launch_bounds__(kSchedThreads) build_schedule_k(const int32_t*
     for (int i = threadIdx.x; i < kCostBuckets; i += kSchedThreads) hist[i] = 0;
     if (threadIdx.x == 0 && counter) *counter = 0;
     __syncthreads();
-    for (int b = threadIdx.x; b < B; b += kSchedThreads) {
+    // one warp per sequence, lanes over its tiles (long sequences have hundreds of tiles)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = warp; b < B; b += kSchedThreads / 32) {
         const int L = offsets[b + 1] - offsets[b];
         const int nt = (L + BMt - 1) / BMt;
-        for (int t = 0; t < nt; ++t) {
+        for (int t = lane; t < nt; t += 32) {
             int c = item_cost(mode, t, L, BMt, BNt, K1, K2);
             atomicAdd(&hist[c < kCostBuckets - 1 ? c : kCostBuckets - 1], 1);
         }
@@ -64,10 +66,10 @@ __global__ void __launch_bounds__(kSchedThreads) build_schedule_k(const int32_t*
         excl += v[i];
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < B; b += kSchedThreads) {
+    for (int b = warp; b < B; b += kSchedThreads / 32) {
         const int o = offsets[b], L = offsets[b + 1] - o;
         const int nt = (L + BMt - 1) / BMt;
-        for (int t = 0; t < nt; ++t) {
+        for (int t = lane; t < nt; t += 32) {
             int c = item_cost(mode, t, L, BMt, BNt, K1, K2);
             int pos = atomicAdd(&hist[c < kCostBuckets - 1 ? c : kCostBuckets - 1], H);
             for (int h = 0; h < H; ++h) items[pos + h] = WorkItem{o, L, t, h};

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* _
     for (int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5); row < nrows;
          row += (int64_t)gridDim.x * kRowsPerBlock) {
         const float mu = mean[row], rs = rstd[row];
-        float xt[CPL][V], g[CPL][V];
+        float xt[CPL][V], g[CPL][V], rr[CPL][V];
         float sg = 0.f, sgx = 0.f;
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* _
                 float xv[V], gv[V], wv[V];
                 Vec<T>::load(x + row * ldx + ch * V, xv);
                 Vec<T>::load(dxh + row * ldg + ch * V, gv);
+                if (dres) Vec<T>::load(dres + row * ldr + ch * V, rr[c]);   // in flight with x, dx^
 #pragma unroll
                 for (int e = 0; e < V; e += 4) load4f(w + ch * V + e, wv + e);
 #pragma unroll
@@ -312,10 +313,9 @@ __global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* _
         for (int c = 0; c < CPL; ++c) {
             int ch = lane + 32 * c;
             if (ch < nch) {
-                float o[V], r[V];
-                if (dres) Vec<T>::load(dres + row * ldr + ch * V, r);
+                float o[V];
 #pragma unroll
-                for (int e = 0; e < V; ++e) o[e] = rs * (g[c][e] - mg - xt[c][e] * mgx) + (dres ? r[e] : 0.f);
+                for (int e = 0; e < V; ++e) o[e] = rs * (g[c][e] - mg - xt[c][e] * mgx) + (dres ? rr[c][e] : 0.f);
                 Vec<T>::store(dx + row * lddx + ch * V, o);
             }
         }
@@ -324,23 +324,51 @@ __global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* _
 }
 
 // ------------------------------------------------------------------ column sums / scale
-// column sums: each thread owns one 16-byte column vector and walks a slice of rows
+// column sums: a block covers cpb 16-byte column vectors x (256 / cpb) row groups; each thread
+// walks its rows with four independent loads in flight, the row groups meet in shared memory,
+// and one atomic per column and block reaches global memory
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_k(int64_t nrows, int n, const T* __restrict__ M, int64_t ldm,
-                                                int64_t rows_per_block, float* out) {
+                                                int64_t rows_per_block, int cpb, float* out) {
     constexpr int V = Vec<T>::N;
-    const int ch = blockIdx.x * 256 + threadIdx.x;
-    if (ch * V >= n) return;
+    __shared__ float red[256 * V];
+    const int rgs = 256 / cpb;
+    const int cl = threadIdx.x % cpb, rg = threadIdx.x / cpb;
+    const int ch = blockIdx.x * cpb + cl;
     const int64_t r0 = blockIdx.y * rows_per_block, r1 = min(nrows, r0 + rows_per_block);
     float s[V] = {};
-    for (int64_t r = r0; r < r1; ++r) {
-        float v[V];
-        Vec<T>::load(M + r * ldm + ch * V, v);
+    if (ch * V < n && rg < rgs) {
+        int64_t r = r0 + rg;
+        for (; r + 3 * rgs < r1; r += 4 * rgs) {
+            float a[V], b[V], c[V], d[V];
+            Vec<T>::load(M + r * ldm + ch * V, a);
+            Vec<T>::load(M + (r + rgs) * ldm + ch * V, b);
+            Vec<T>::load(M + (r + 2 * rgs) * ldm + ch * V, c);
+            Vec<T>::load(M + (r + 3 * rgs) * ldm + ch * V, d);
 #pragma unroll
-        for (int e = 0; e < V; ++e) s[e] += v[e];
+            for (int e = 0; e < V; ++e) s[e] += (a[e] + b[e]) + (c[e] + d[e]);
+        }
+        for (; r < r1; r += rgs) {
+            float a[V];
+            Vec<T>::load(M + r * ldm + ch * V, a);
+#pragma unroll
+            for (int e = 0; e < V; ++e) s[e] += a[e];
+        }
     }
+    if (rgs > 1) {
 #pragma unroll
-    for (int e = 0; e < V; ++e) atomicAdd(out + ch * V + e, s[e]);
+        for (int e = 0; e < V; ++e) red[threadIdx.x * V + e] = s[e];
+        __syncthreads();
+        if (rg == 0) {
+            for (int g = 1; g < rgs; ++g)
+#pragma unroll
+                for (int e = 0; e < V; ++e) s[e] += red[(g * cpb + cl) * V + e];
+        }
+    }
+    if (rg == 0 && ch * V < n) {
+#pragma unroll
+        for (int e = 0; e < V; ++e) atomicAdd(out + ch * V + e, s[e]);
+    }
 }
 
 template <typename T>
@@ -453,13 +481,16 @@ uh_status ln_bwd(uh_dtype dt, int64_t T_, int d, const void* dxh, int64_t ldg, c
 uh_status colsum(uh_dtype dt, int64_t T_, int n, const void* M, int64_t ldm, float* out, cudaStream_t st) {
     if (T_ == 0 || n == 0) return UH_OK;
     const int V = dt == UH_BF16 ? 8 : 4;
-    const int64_t cols_blocks = (n / V + 255) / 256;
-    int64_t ry = (8 * num_sms() + cols_blocks - 1) / cols_blocks;
+    const int nch = (n + V - 1) / V;
+    int cpb = nch < 256 ? nch : 256;
+    while (256 % cpb) ++cpb;                     // row groups tile the block exactly
+    const int64_t cols_blocks = (nch + cpb - 1) / cpb;
+    int64_t ry = (4 * num_sms() + cols_blocks - 1) / cols_blocks;
     int64_t rpb = (T_ + ry - 1) / ry;
-    if (rpb < 32) rpb = 32;
+    if (rpb < 64) rpb = 64;
     ry = (T_ + rpb - 1) / rpb;
     dim3 grid((unsigned)cols_blocks, (unsigned)ry);
-    UH_DT_DISPATCH(dt, colsum_k<T><<<grid, 256, 0, st>>>(T_, n, (const T*)M, ldm, rpb, out));
+    UH_DT_DISPATCH(dt, colsum_k<T><<<grid, 256, 0, st>>>(T_, n, (const T*)M, ldm, rpb, cpb, out));
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
