@@ -149,7 +149,6 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const WorkItem it = a.items[w];
             const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
             const int n = key_tiles_count(kt);
-            const int kc0 = kc, g0 = sc;
             mbar_wait(&bars->qa_full, qi & 1);
             tc_fence_after();
             if (elect_one()) {   // Q, dA: smem -> TMEM (ordered with the MMAs of the previous item)
@@ -162,47 +161,61 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 umma_commit(&bars->qa_empty);
             }
             __syncwarp();
+            // S(j) / dP(j) run one tile ahead of dQ(j - 1).  The next block's barrier is probed
+            // (test_wait) before the current block's MMAs are issued and waited on after them.
+            int s_st = kc % STAGES, s_ph = (kc / STAGES) & 1, s_sb = sc & 1;
+            int p_st = s_st, p_b = sc & 1, p_ph = (sc >> 1) & 1;
+            mbar_wait(&bars->kv_full[s_st], s_ph);
             for (int j = 0; j <= n; ++j) {
                 if (j < n) {   // ---- S(j) = Q K_j^T, dP(j) = dA V_j^T
-                    const int s = kc % STAGES, sb = sc % NS;
-                    if (lane == 0) TRACE(0 * 1024 + (sc & 1023));
-                    mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
                     tc_fence_after();
-                    if (lane == 0) TRACE(1 * 1024 + (sc & 1023));
+                    // next block: dQ(j - 1) if j >= 1, else S(1) if n > 1, else dQ(0)
+                    const bool nxt_p = j >= 1 || n == 1;
+                    const int ns_st = s_st + 1 == STAGES ? 0 : s_st + 1, ns_ph = s_st + 1 == STAGES ? s_ph ^ 1 : s_ph;
+                    uint64_t* nb = nxt_p ? &bars->ds_full[p_b] : &bars->kv_full[ns_st];
+                    const uint32_t np = nxt_p ? p_ph : ns_ph;
+                    const bool rdy = mbar_test(smem_u32(nb), np);
                     if (elect_one()) {
-                        const uint32_t k_addr = smem_u32(sKV + s * 2 * KT), v_addr = k_addr + KT;
+                        const uint32_t k_addr = smem_u32(sKV + s_st * 2 * KT), v_addr = k_addr + KT;
 #pragma unroll
                         for (int kk = 0; kk < DH / 16; ++kk) {
                             const uint32_t ob = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
-                            umma_ts(tmem + S_COL + sb * BN, tmem + Q_COL + kk * 8, make_sw128_desc(k_addr + ob, 16, 1024),
+                            umma_ts(tmem + S_COL + s_sb * BN, tmem + Q_COL + kk * 8, make_sw128_desc(k_addr + ob, 16, 1024),
                                     idesc_s, kk > 0 ? 1u : 0u);
-                            umma_ts(tmem + DP_COL + sb * BN, tmem + DA_COL + kk * 8,
+                            umma_ts(tmem + DP_COL + s_sb * BN, tmem + DA_COL + kk * 8,
                                     make_sw128_desc(v_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
                         }
-                        umma_commit(&bars->s_full[sb]);
+                        umma_commit(&bars->s_full[s_sb]);
                     }
                     __syncwarp();
+                    s_st = ns_st; s_ph = ns_ph; s_sb ^= 1;
                     ++kc; ++sc;
+                    if (!rdy) mbar_wait(nb, np);
                 }
                 if (j >= 1) {  // ---- dQ += dS(jj) K_jj  (dS over the consumed S columns)
-                    const int jj = j - 1, g = g0 + jj;
-                    const int stage = (kc0 + jj) % STAGES, db = g % NS;
+                    const int jj = j - 1;
                     if (jj == 0) mbar_wait(&bars->dq_empty, (qi & 1) ^ 1);
-                    if (lane == 0) TRACE(2 * 1024 + (g & 1023));
-                    mbar_wait(&bars->ds_full[db], (g / NS) & 1);
                     tc_fence_after();
-                    if (lane == 0) TRACE(3 * 1024 + (g & 1023));
+                    // next block: S(j + 1) if it exists, else dQ(j) if it exists, else none
+                    const bool nxt_s = j + 1 < n;
+                    const int np_b = p_b ^ 1, np_ph = p_b == 1 ? p_ph ^ 1 : p_ph;
+                    uint64_t* nb = nxt_s ? &bars->kv_full[s_st] : &bars->ds_full[j < n ? np_b : p_b];
+                    const uint32_t np = nxt_s ? s_ph : (j < n ? np_ph : p_ph);
+                    const bool rdy = mbar_test(smem_u32(nb), np);
                     if (elect_one()) {
-                        const uint32_t k_addr = smem_u32(sKV + stage * 2 * KT);
+                        const uint32_t k_addr = smem_u32(sKV + p_st * 2 * KT);
 #pragma unroll
                         for (int kk = 0; kk < BN / 16; ++kk)
-                            umma_ts(tmem + DQ_COL, tmem + S_COL + db * BN + (kk >> 1) * 32 + (kk & 1) * 8,
+                            umma_ts(tmem + DQ_COL, tmem + S_COL + p_b * BN + (kk >> 1) * 32 + (kk & 1) * 8,
                                     make_sw128_desc(k_addr + kk * 2048, KT / 2, 1024), idesc_q,
                                     (jj > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit(&bars->kv_empty[stage]);
+                        umma_commit(&bars->kv_empty[p_st]);
                         if (jj == n - 1) umma_commit(&bars->dq_full);
                     }
                     __syncwarp();
+                    p_st = p_st + 1 == STAGES ? 0 : p_st + 1;
+                    p_b = np_b; p_ph = np_ph;
+                    if (!rdy) mbar_wait(nb, np);
                 }
             }
         }
@@ -515,13 +528,16 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 const int kb = ki & 1;
                 const uint64_t dk = kv_k + ((uint32_t)(kb * 2 * KT) >> 4), dv = dk + (KT >> 4);
                 mbar_wait(&bars->kv_full[kb], (ki >> 1) & 1);
+                mbar_wait(&bars->qa_full[st_s], ph_s);
+                mbar_wait(&bars->issued[sc & 1], ((sc >> 1) - 1) & 1);   // (first steps: parity 1 of a fresh barrier passes)
                 for (int i = 0; i < n; ++i, ++sc) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
                     const int sb = sc & 1;
-                    if (lane == 0) TRACE_DKV(0 * 1024 + (sc & 1023));
-                    mbar_wait(&bars->qa_full[st_s], ph_s);
-                    if (sc >= NS) mbar_wait(&bars->issued[sb], ((sc >> 1) - 1) & 1);
                     tc_fence_after();
-                    if (lane == 0) TRACE_DKV(1 * 1024 + (sc & 1023));
+                    // probe step i+1's barriers now, wait on them after this step's MMAs are issued
+                    const int nst = st_s + 1 == STAGES ? 0 : st_s + 1, nph = st_s + 1 == STAGES ? ph_s ^ 1 : ph_s;
+                    const uint32_t qa_a = smem_u32(&bars->qa_full[nst]), is_a = smem_u32(&bars->issued[sb ^ 1]);
+                    const uint32_t is_p = (((sc + 1) >> 1) - 1) & 1;
+                    const bool r1 = mbar_test(qa_a, nph), r2 = mbar_test(is_a, is_p);
                     const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
                     const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
                     if (elect_one()) {
@@ -536,8 +552,11 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                         if (i == n - 1) umma_commit(&bars->kv_empty[kb]);   // K, V read by the last S^T / dP^T
                     }
                     __syncwarp();
-                    if (lane == 0) TRACE_DKV(2 * 1024 + (sc & 1023));
-                    if (++st_s == STAGES) { st_s = 0; ph_s ^= 1; }
+                    st_s = nst; ph_s = nph;
+                    if (i + 1 < n) {
+                        if (!r1) mbar_wait_addr(qa_a, nph);
+                        if (!r2) mbar_wait_addr(is_a, is_p);
+                    }
                 }
             }
         } else {
@@ -548,13 +567,13 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 if (w < 0) break;
                 const WorkItem it = a.items[w];
                 const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+                mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
+                mbar_wait(&bars->p_full[sc & 1], (sc >> 1) & 1);
                 for (int i = 0; i < n; ++i, ++sc) {   // ---- dV += P^T dA, dK += dS^T Q
                     const int pb = sc & 1;
-                    if (i == 0) mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
-                    if (lane == 0) TRACE_DKV(3 * 1024 + (sc & 1023));
-                    mbar_wait(&bars->p_full[pb], (sc >> 1) & 1);
                     tc_fence_after();
-                    if (lane == 0) TRACE_DKV(4 * 1024 + (sc & 1023));
+                    const uint32_t pf_a = smem_u32(&bars->p_full[pb ^ 1]), pf_p = ((sc + 1) >> 1) & 1;
+                    const bool r = mbar_test(pf_a, pf_p);   // step i+1's P^T / dS^T
                     const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
                     const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
                     if (elect_one()) {
@@ -572,8 +591,8 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->issued[pb]);
-                    if (lane == 0) TRACE_DKV(5 * 1024 + (sc & 1023));
                     if (++st_a == STAGES) st_a = 0;
+                    if (i + 1 < n && !r) mbar_wait_addr(pf_a, pf_p);
                 }
             }
         }

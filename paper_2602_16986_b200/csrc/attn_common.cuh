@@ -51,6 +51,19 @@ struct AttnArgs {
     int* counter;                          // dynamic work counter (persistent kernels)
 };
 
+// MMA block order of one item with n tiles whose second block (PV / dQ / dV-dK) runs LAG
+// tiles behind its first (S, or S and dP): S0 .. S(LAG-1), then S(j) P(j-LAG) pairs, then
+// the remaining P blocks.  Lets the issuer name (and probe) the barrier of block k+1.
+struct MmaBlk { int tile; bool first; };
+UH_HD MmaBlk lag_block(int k, int n, int lag) {
+    const int h = n < lag ? n : lag;
+    if (k < h) return {k, true};
+    int r = k - h;
+    const int pairs = n > lag ? n - lag : 0;
+    if (r < 2 * pairs) return {(r & 1) ? (r >> 1) : lag + (r >> 1), !(r & 1)};
+    return {pairs + (r - 2 * pairs), false};
+}
+
 // Dynamic work distribution for the persistent tcgen05 kernels: the producer lane claims
 // the next item of the cost-descending list (F0) with one atomicAdd, so the list is served
 // longest-first to whichever CTA frees up (LPT), and publishes it to the CTA's other roles

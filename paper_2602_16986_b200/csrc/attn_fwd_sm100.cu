@@ -111,6 +111,9 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     const int s = kc % STAGES;
                     uint8_t* st = sKV + s * 2 * KT;
                     mbar_wait_sleep(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
+#if UH_EXP == 3
+                    mbar_arrive(&bars->kv_full[s]); ++kc; continue;
+#endif
                     mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
                     tma_load_2d(st, &tmK, &bars->kv_full[s], h * DH, row);
                     tma_load_2d(st + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
@@ -143,47 +146,64 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 umma_commit(&bars->q_empty);
             }
             __syncwarp();
+            // S(j) runs LAG tiles ahead of PV(j - LAG).  The barrier of the next block is probed
+            // (mbarrier.test_wait, never parks) just before the current block's MMAs are issued and
+            // only then waited on, so an already-complete barrier costs no pipe idle time.
+            // Incremental ring state: S side (kv stage / phase, S buffer), PV side (kv stage,
+            // P buffer / phase).
+            int s_st = kc % STAGES, s_ph = (kc / STAGES) & 1, s_sb = sc % NS;
+            int p_st = s_st, p_b = pc % NS, p_ph = (pc / NS) & 1;
+            mbar_wait(&bars->kv_full[s_st], s_ph);
             for (int j = 0; j < n + LAG; ++j) {
-                if (j < n) {   // ---- S(j) = Q K_j^T
-                    // buffer sb was last read by PV(j - NS), issued earlier: the tensor pipe is in order
-                    const int s = kc % STAGES, sb = sc % NS;
-                    mbar_wait(&bars->kv_full[s], (kc / STAGES) & 1);
-                    if (lane == 0) TRACE(0 * 1024 + sc);
+                if (j < n) {   // ---- S(j) = Q K_j^T  (buffer s_sb last read by PV(j - NS): the pipe is in order)
                     tc_fence_after();
+                    // next block: PV(j - LAG) if it exists, else S(j + 1), else PV(0) (n <= LAG)
+                    const bool nxt_p = j >= LAG || j + 1 >= n;
+                    const int ns_st = s_st + 1 == STAGES ? 0 : s_st + 1, ns_ph = s_st + 1 == STAGES ? s_ph ^ 1 : s_ph;
+                    uint64_t* nb = nxt_p ? &bars->p_full[p_b] : &bars->kv_full[ns_st];
+                    const uint32_t np = nxt_p ? p_ph : ns_ph;
+                    const bool rdy = mbar_test(smem_u32(nb), np);
                     if (elect_one()) {
-                        const uint32_t k_addr = smem_u32(sKV + s * 2 * KT);
+                        const uint32_t k_addr = smem_u32(sKV + s_st * 2 * KT);
 #pragma unroll
                         for (int kk = 0; kk < DH / 16; ++kk)
-                            umma_ts(tmem + sb * BN, tmem + Q_COL + kk * 8,
+                            umma_ts(tmem + s_sb * BN, tmem + Q_COL + kk * 8,
                                     make_sw128_desc(k_addr + (kk >> 2) * (KT / 2) + (kk & 3) * 32, 16, 1024), idesc_s,
                                     kk > 0 ? 1u : 0u);
-                        umma_commit(&bars->s_full[sb]);
+                        umma_commit(&bars->s_full[s_sb]);
                     }
                     __syncwarp();
-                    ++sc; ++kc;
+                    s_st = ns_st; s_ph = ns_ph;
+                    s_sb = s_sb + 1 == NS ? 0 : s_sb + 1;
+                    if (!rdy) mbar_wait(nb, np);
                 }
-                if (j >= LAG) {   // ---- O += P(jj) V_jj
+                if (j >= LAG) {   // ---- O += P(jj) V_jj  (P over the consumed S columns: keys [32g, 32g+32) at col 32g)
                     const int jj = j - LAG;
-                    const int stage = (kc0 + jj) % STAGES, pb = pc % NS;
                     if (jj == 0) mbar_wait(&bars->o_empty, (qi & 1) ^ 1);
-                    mbar_wait(&bars->p_full[pb], (pc / NS) & 1);
-                    if (lane == 0) TRACE(1 * 1024 + pc);
                     tc_fence_after();
+                    // next block: S(j + 1) if it exists, else PV(jj + 1) if it exists, else none
+                    const bool nxt_s = j + 1 < n;
+                    const int np_b = p_b + 1 == NS ? 0 : p_b + 1, np_ph = p_b + 1 == NS ? p_ph ^ 1 : p_ph;
+                    uint64_t* nb = nxt_s ? &bars->kv_full[s_st] : &bars->p_full[jj + 1 < n ? np_b : p_b];
+                    const uint32_t np = nxt_s ? s_ph : (jj + 1 < n ? np_ph : p_ph);
+                    const bool rdy = mbar_test(smem_u32(nb), np);
                     if (elect_one()) {
-                        // P(jj) lives in TMEM over the consumed S columns: keys [32g, 32g+32) at column 32g
-                        const uint32_t v_addr = smem_u32(sKV + stage * 2 * KT + KT);
+                        const uint32_t v_addr = smem_u32(sKV + p_st * 2 * KT + KT);
 #pragma unroll
                         for (int kk = 0; kk < BN / 16; ++kk)
-                            umma_ts(tmem + O_COL, tmem + pb * BN + (kk >> 1) * 32 + (kk & 1) * 8,
+                            umma_ts(tmem + O_COL, tmem + p_b * BN + (kk >> 1) * 32 + (kk & 1) * 8,
                                     make_sw128_desc(v_addr + kk * 2048, KT / 2, 1024), idesc_o,
                                     (jj > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit(&bars->kv_empty[stage]);
+                        umma_commit(&bars->kv_empty[p_st]);
                         if (jj == n - 1) umma_commit(&bars->o_full);
                     }
                     __syncwarp();
-                    ++pc;
+                    p_st = p_st + 1 == STAGES ? 0 : p_st + 1;
+                    p_b = np_b; p_ph = np_ph;
+                    if (!rdy) mbar_wait(nb, np);
                 }
             }
+            kc += n; sc += n; pc += n;
         }
     } else if (warp >= 4) {
         // ============================================================ epilogue
@@ -216,6 +236,10 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
                 if (warp == 4 && lane == 0) TRACE(3 * 1024 + (sc & 1023));
                 tc_fence_after();
+#if UH_EXP == 1 || UH_EXP == 3
+                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+                continue;
+#endif
 #pragma unroll
                 for (int hc = 0; hc < 2; ++hc) {
                     const int kb = k0 + 32 * hc;

@@ -48,6 +48,19 @@ UH_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
     return ok != 0;
 }
+// Non-blocking probe of a phase (never parks the thread).  The MMA issuers probe the next
+// block's barrier just before issuing the current block: the probe's latency (~130-150
+// cycles, also for an already-complete phase) then overlaps the tcgen05.mma issue instead
+// of draining the 4-5 deep MMA queue.
+UH_DEV bool mbar_test(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+    return ok != 0;
+}
 // try_wait with a suspend-time hint (ns): the thread sleeps until the phase completes or
 // the hint elapses, instead of re-polling and taking issue slots from co-resident warps.
 UH_DEV bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
@@ -66,6 +79,12 @@ UH_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     uint32_t n = 0;
     while (!mbar_try_wait_sleep(addr, parity)) {
         if (++n > 400000u) __trap();
+    }
+}
+UH_DEV void mbar_wait_addr(uint32_t addr, uint32_t parity) {
+    uint32_t n = 0;
+    while (!mbar_try_wait(addr, parity)) {
+        if (++n > 400000000u) __trap();
     }
 }
 // Blocking wait on the phase with the given parity.  A wait that never completes
