@@ -203,6 +203,9 @@ UH_API uh_status uh_layer_bwd(const uh_jagged* jag, uh_mask m, const uh_layer_pa
 
 /* ---------------------------------------------------------------------------
  * Jagged gather / scatter (P:190 jagged tensors).
+ * Row bytes (width * elem_bytes) must be a multiple of 8 and x / y 16-byte
+ * aligned (UH_ERR_ALIGNMENT); 16-byte multiples take the vectorised path, 8-byte
+ * rows (e.g. int64 timestamps, width 1) one lane per row.
  * ------------------------------------------------------------------------- */
 /* Pack the rows of sequences seq_ids_host[0..n) of `src` (row width `width`
  * elements of `elem_bytes` bytes, row stride ld_x) contiguously into y (row

@@ -14,31 +14,40 @@ constexpr int kSegs = 256;  // segments per launch (kernel-parameter budget)
 struct Seg { int32_t src, dst, len; };
 struct SegBatch { Seg s[kSegs]; int n; };
 
-// copy `len` rows per segment; row bytes multiple of 16
+// copy `len` rows per segment with VT-wide vectors (uint4: row bytes multiple of 16; uint2:
+// multiple of 8, e.g. int64 timestamps)
+template <typename VT>
 __global__ void __launch_bounds__(256) copy_rows_k(SegBatch b, const uint8_t* __restrict__ x, int64_t ldx_bytes,
                                                    uint8_t* __restrict__ y, int64_t ldy_bytes, int64_t row_bytes) {
     const int seg = blockIdx.y;
     if (seg >= b.n) return;
     const Seg s = b.s[seg];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nvec = row_bytes / 16;
+    const int64_t nvec = row_bytes / (int64_t)sizeof(VT);
+    if (nvec == 1) {   // narrow rows: one lane per row
+        for (int r = (blockIdx.x * 8 + warp) * 32 + lane; r < s.len; r += gridDim.x * 256)
+            *reinterpret_cast<VT*>(y + (int64_t)(s.dst + r) * ldy_bytes) =
+                *reinterpret_cast<const VT*>(x + (int64_t)(s.src + r) * ldx_bytes);
+        return;
+    }
     for (int r = blockIdx.x * 8 + warp; r < s.len; r += gridDim.x * 8) {
-        const uint4* src = reinterpret_cast<const uint4*>(x + (int64_t)(s.src + r) * ldx_bytes);
-        uint4* dst = reinterpret_cast<uint4*>(y + (int64_t)(s.dst + r) * ldy_bytes);
+        const VT* src = reinterpret_cast<const VT*>(x + (int64_t)(s.src + r) * ldx_bytes);
+        VT* dst = reinterpret_cast<VT*>(y + (int64_t)(s.dst + r) * ldy_bytes);
         for (int64_t v = lane; v < nvec; v += 32) dst[v] = src[v];
     }
 }
 
+template <typename VT>
 __global__ void __launch_bounds__(256) zero_rows_k(SegBatch b, uint8_t* __restrict__ y, int64_t ldy_bytes,
                                                    int64_t row_bytes) {
     const int seg = blockIdx.y;
     if (seg >= b.n) return;
     const Seg s = b.s[seg];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nvec = row_bytes / 16;
+    const int64_t nvec = row_bytes / (int64_t)sizeof(VT);
     for (int r = blockIdx.x * 8 + warp; r < s.len; r += gridDim.x * 8) {
-        uint4* dst = reinterpret_cast<uint4*>(y + (int64_t)(s.dst + r) * ldy_bytes);
-        for (int64_t v = lane; v < nvec; v += 32) dst[v] = make_uint4(0, 0, 0, 0);
+        VT* dst = reinterpret_cast<VT*>(y + (int64_t)(s.dst + r) * ldy_bytes);
+        for (int64_t v = lane; v < nvec; v += 32) dst[v] = VT{};
     }
 }
 
@@ -52,8 +61,12 @@ uh_status run_segments(const std::vector<Seg>& segs, const void* x, int64_t ldx_
         b.n = (int)std::min<size_t>(kSegs, segs.size() - i0);
         for (int i = 0; i < b.n; ++i) b.s[i] = segs[i0 + i];
         dim3 grid((unsigned)std::min(64, (maxlen + 7) / 8), (unsigned)b.n);
-        if (zero) zero_rows_k<<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
-        else copy_rows_k<<<grid, 256, 0, st>>>(b, (const uint8_t*)x, ldx_bytes, (uint8_t*)y, ldy_bytes, row_bytes);
+        if (zero && row_bytes % 16 == 0) zero_rows_k<uint4><<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
+        else if (zero) zero_rows_k<uint2><<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
+        else if (row_bytes % 16 == 0)
+            copy_rows_k<uint4><<<grid, 256, 0, st>>>(b, (const uint8_t*)x, ldx_bytes, (uint8_t*)y, ldy_bytes, row_bytes);
+        else
+            copy_rows_k<uint2><<<grid, 256, 0, st>>>(b, (const uint8_t*)x, ldx_bytes, (uint8_t*)y, ldy_bytes, row_bytes);
         note_launch();
         UH_CUDA(cudaGetLastError());
     }
@@ -65,7 +78,7 @@ uh_status check_common(const uh_jagged* j, const void* x, int64_t width, int32_t
     if (j->num_seqs < 0) return fail(UH_ERR_DOMAIN, "num_seqs < 0");
     if (eb != 1 && eb != 2 && eb != 4 && eb != 8) return fail(UH_ERR_DOMAIN, "elem_bytes must be 1, 2, 4 or 8");
     if (width < 0) return fail(UH_ERR_DOMAIN, "width < 0");
-    if ((width * eb) % 16) return fail(UH_ERR_ALIGNMENT, "row bytes must be a multiple of 16");
+    if ((width * eb) % 8) return fail(UH_ERR_ALIGNMENT, "row bytes must be a multiple of 8");
     if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15)
         return fail(UH_ERR_ALIGNMENT, "x / y not 16-byte aligned");
     for (int b = 0; b < j->num_seqs; ++b)
@@ -93,7 +106,7 @@ uh_status uh_jagged_gather(const uh_jagged* src, const int32_t* seq_ids, int32_t
     UH_TRY(check_common(src, x, width, eb, y));
     if (n < 0) return fail(UH_ERR_DOMAIN, "n < 0");
     if (n > 0 && !seq_ids) return fail(UH_ERR_NULL, "seq_ids NULL");
-    if (ld_x < width || (ld_x * eb) % 16) return fail(UH_ERR_ALIGNMENT, "ld_x");
+    if (ld_x < width || (ld_x * eb) % 8) return fail(UH_ERR_ALIGNMENT, "ld_x (bytes) must be a multiple of 8");
     std::vector<Seg> segs;
     std::vector<int32_t> off(1, 0);
     for (int i = 0; i < n; ++i) {
@@ -111,7 +124,7 @@ uh_status uh_jagged_slice_latest(const uh_jagged* src, int32_t l_keep, const voi
                                  int32_t eb, void* y, int32_t* dst_off_host, int32_t* dst_off_dev, void* stream) {
     UH_TRY(check_common(src, x, width, eb, y));
     if (l_keep < 0) return fail(UH_ERR_DOMAIN, "l_keep < 0");
-    if (ld_x < width || (ld_x * eb) % 16) return fail(UH_ERR_ALIGNMENT, "ld_x");
+    if (ld_x < width || (ld_x * eb) % 8) return fail(UH_ERR_ALIGNMENT, "ld_x (bytes) must be a multiple of 8");
     std::vector<Seg> segs;
     std::vector<int32_t> off(1, 0);
     for (int b = 0; b < src->num_seqs; ++b) {

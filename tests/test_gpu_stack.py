@@ -1,0 +1,62 @@
+"""NEXT-1: the inference schedule with attention truncation — SLA layers on
+the whole jagged sequences, then the latest L' tokens of each sequence (uh_jagged_slice_latest,
+P:198-199) through full-causal layers — against the oracle composed layer by layer
+(numpy slicing of the oracle's own rows and timestamps).  bf16 bar 2e-2 per tensor."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import rel_inf, to_dev, to_np
+from paper_2602_16986_b200 import stack as S
+from paper_2602_16986_b200 import synth
+from paper_2602_16986_b200 import uhstu as U
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("l_keep", [256, 64])
+def test_truncated_inference_stack(l_keep):
+    lengths = [300, 700, 1200, 64, 5]
+    H, dh = 2, 128
+    d = H * dh
+    n_full, n_trunc = 2, 2
+    K1, K2, N_full = 128, 16, 1200.0
+    cfg = synth.Config("stack", lengths, H=H, dh=dh, K1=K1, K2=K2, N=N_full, seed=5, pos_len=64)
+    x, _ = synth.layer_inputs(cfg)
+    pos, ts = synth.rab_tables(cfg)
+    t = synth.timestamps(cfg.seed, lengths)
+    params = [synth.layer_params(d, cfg.seed, layer=l) for l in range(n_full + n_trunc)]
+
+    # ---- GPU: one call per layer through the C ABI
+    f = lambda a: torch.from_numpy(a).cuda()
+    w = lambda a: torch.from_numpy(a).to("cuda", torch.bfloat16)
+    layers = []
+    for l, p in enumerate(params):
+        prm = U.Params(f(p["ln1_w"]), f(p["ln1_b"]), w(p["w1"]), f(p["ln2_w"]), f(p["ln2_b"]), w(p["w2"]),
+                       f(p["b1"]), f(p["b2"]))
+        attn = U.Attn(H, dh, 1.0, N_full, f(pos), f(ts), f(t))
+        m = U.mask(K1, K2) if l < n_full else U.mask()
+        layers.append(S.Layer(prm, attn, m))
+    jag = U.JaggedBatch(cfg.offsets())
+    out, jt = S.forward_truncated(jag, to_dev(x, U.BF16), layers, n_full, l_keep, norm_n_truncated=float(l_keep))
+    torch.cuda.synchronize()
+
+    # ---- oracle: the same schedule, layer by layer in fp64
+    off = cfg.offsets()
+    h = x.astype(np.float64)
+    for l in range(n_full):
+        prm = O.LayerParams(**{k: np.asarray(v, np.float64) for k, v in params[l].items()})
+        spec = O.AttnSpec(K1=K1, K2=K2, alpha=1.0, N=N_full, pos_w=pos, ts_w=ts, timestamps=t)
+        h, _ = O.layer_forward(h, off, prm, H, spec)
+    keep = np.concatenate([np.arange(off[b + 1] - min(l_keep, L), off[b + 1]) for b, L in enumerate(lengths)])
+    lk = [min(l_keep, L) for L in lengths]
+    off2 = np.zeros(len(lk) + 1, np.int32)
+    off2[1:] = np.cumsum(lk)
+    assert list(jt.lengths) == lk
+    h, t2 = h[keep], t[keep]
+    for l in range(n_full, n_full + n_trunc):
+        prm = O.LayerParams(**{k: np.asarray(v, np.float64) for k, v in params[l].items()})
+        spec = O.AttnSpec(K1=O.FULL, K2=0, alpha=1.0, N=float(l_keep), pos_w=pos, ts_w=ts, timestamps=t2)
+        h, _ = O.layer_forward(h, off2, prm, H, spec)
+    assert rel_inf(to_np(out), h) <= 2e-2
