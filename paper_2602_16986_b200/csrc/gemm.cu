@@ -102,9 +102,9 @@ static uh_status gemm_f32(const GemmDesc& g, cudaStream_t st) {
 }
 
 // ============================================================== bf16 tcgen05
-template <int BN, bool AMN, bool BMN, int EPI>
+template <int BN, bool AMN, bool BMN, int EPI, int MSUB = 1>
 static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, MSUB, EPI>;
     CUtensorMap ta, tb;
     if (!AMN) UH_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, C::BM));
     else      UH_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
@@ -132,7 +132,7 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     a.out0 = g.out0; a.ld0 = g.ld0; a.out1 = g.out1; a.ld1 = g.ld1;
     a.bias = g.bias; a.resid = (const __nv_bfloat16*)g.resid; a.ldr = g.ldr;
     const int total = a.m_tiles * a.n_tiles * a.k_splits;
-    auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI>;
+    auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI, MSUB>;
     UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     kern<<<std::min(total, sms), 384, C::SMEM, st>>>(ta, tb, to0, to1, a);
     note_launch();
@@ -148,6 +148,8 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
     const bool wide = g.N % 256 == 0 && g.epi != EPI_F32;
 #define UH_G(BN, AM, BM_, E) return launch_sm100<BN, AM, BM_, E>(g, st)
     if (g.epi == EPI_F32) {
+        // weight gradients (K = tokens): 256 x 256 tiles (two 128-row sub-tiles share each B k-block)
+        if (g.a_mn && g.b_mn && g.M % 256 == 0 && g.N % 256 == 0) return launch_sm100<256, true, true, EPI_F32, 2>(g, st);
         if (g.a_mn && g.b_mn) UH_G(128, true, true, EPI_F32);
         if (!g.a_mn && !g.b_mn) UH_G(128, false, false, EPI_F32);
         return fail(UH_ERR_UNSUPPORTED, "gemm EPI_F32 with mixed majors");

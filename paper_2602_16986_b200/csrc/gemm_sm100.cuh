@@ -33,23 +33,28 @@ struct GemmArgs {
     const __nv_bfloat16* resid; int64_t ldr;
 };
 
-template <int BN>
+// MSUB row sub-tiles of 128 share each B k-block (tile BM = 128 MSUB): for the long-K split-K
+// weight gradients, a 256 x 256 tile streams 64 KB per 1024 MMA cycles instead of 128 x 128's
+// 32 KB per 256 (L2->SM ingress is the limit there).  NACC TMEM accumulators (2 when they fit:
+// the epilogue of tile i overlaps tile i+1's main loop).
+template <int BN, int MSUB = 1, int EPI = 0>
 struct GemmCfg {
-    static constexpr int BM = 128, BK = 64;
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int BM = 128 * MSUB, BK = 64;
+    static constexpr int STAGES = MSUB == 2 ? 3 : (BN == 256 ? 4 : 6);
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGING = 8 * 2 * 2048;   // per epilogue warp: a 32x32 bf16 box per output
+    static constexpr int STAGING = EPI == 2 ? 0 : 8 * 2 * 2048;   // per epilogue warp: a 32x32 bf16 box per output
     static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+    static constexpr int NACC = 2 * MSUB * BN <= 512 ? 2 : 1;
+    static constexpr int TMEM_COLS = NACC * MSUB * BN <= 256 ? 256 : 512;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int MSUB = 1>
 __global__ void __launch_bounds__(384, 1)
 gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1, GemmArgs g) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, MSUB, EPI>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -121,17 +126,17 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = make_idesc_bf16(C::BM, BN, A_MN, B_MN);
+        constexpr uint32_t idesc = make_idesc_bf16(128, BN, A_MN, B_MN);
         int stage = 0; uint32_t phase = 0;
         int it = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
             int mt, nt, ks, kb0, kb1;
             decode(t, mt, nt, ks);
             kb_range(ks, kb0, kb1);
-            const int acc = it & 1;
-            mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+            const int acc = C::NACC == 2 ? (it & 1) : 0;
+            mbar_wait(&tempty[acc], (C::NACC == 2 ? ((it >> 1) & 1) : (it & 1)) ^ 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
+            const uint32_t d_tmem = tmem_base + acc * MSUB * BN;
             for (int kb = kb0; kb < kb1; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
@@ -140,11 +145,14 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < C::BK / 16; ++k) {
-                        uint64_t ad = A_MN ? make_sw128_desc(a0 + k * 2048, 64 * C::BK * 2, 1024)
-                                           : make_sw128_desc(a0 + k * 32, 16, 1024);
                         uint64_t bd = B_MN ? make_sw128_desc(b0 + k * 2048, 64 * C::BK * 2, 1024)
                                            : make_sw128_desc(b0 + k * 32, 16, 1024);
-                        umma_ss(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+#pragma unroll
+                        for (int ms = 0; ms < MSUB; ++ms) {   // rows [128 ms, 128 ms + 128) start 16 KB apart (both majors)
+                            uint64_t ad = A_MN ? make_sw128_desc(a0 + ms * 16384 + k * 2048, 64 * C::BK * 2, 1024)
+                                               : make_sw128_desc(a0 + ms * 16384 + k * 32, 16, 1024);
+                            umma_ss(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     umma_commit(&empty[stage]);
                 }
@@ -163,15 +171,17 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
             int mt, nt, ks;
             decode(t, mt, nt, ks);
-            const int acc = it & 1;
-            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            const int acc = C::NACC == 2 ? (it & 1) : 0;
+            mbar_wait(&tfull[acc], C::NACC == 2 ? ((it >> 1) & 1) : (it & 1));
             tc_fence_after();
-            const int row = mt * C::BM + row_in_tile;
+#pragma unroll 1
+            for (int ms = 0; ms < MSUB; ++ms) {
+            const int row = mt * C::BM + ms * 128 + row_in_tile;
             const bool row_ok = row < g.M;
 #pragma unroll 1
             for (int c0 = wg * (BN / 2); c0 < (wg + 1) * (BN / 2); c0 += 32) {
                 float v[32];
-                tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + c0, v);
+                tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + (acc * MSUB + ms) * BN + c0, v);
                 tmem_ld_wait();
                 const int col = nt * BN + c0;
                 if (col >= g.N) continue;   // warp-uniform
@@ -244,13 +254,14 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane_id() == 0) {
-                        const int row0 = mt * C::BM + wq * 32;
+                        const int row0 = mt * C::BM + ms * 128 + wq * 32;
                         tma_store_2d(&tmO0, box0, col, row0);
                         if (EPI == EPI_SILU && g.out1) tma_store_2d(&tmO1, box1, col, row0);
                         bulk_commit();
                     }
                 }
             }
+            }   // ms
             tc_fence_before();
             __syncwarp();
             if (lane_id() == 0) mbar_arrive(&tempty[acc]);
