@@ -14,7 +14,7 @@ from attn_time import run
 run(B=int(sys.argv[2]) if len(sys.argv) > 2 else 2, rab=bool(int(sys.argv[1])) if len(sys.argv) > 1 else False, steps=1)
 t = buf.view(8, 1024).cpu().numpy()
 t0 = t[t > 0].min()
-names = ["w1_beg", "w1_got", "w1_end", "w3_beg", "w3_got", "w3_end", "wg0_arr", "wg1_arr"]
+names = ["w1_beg", "w1_lastS", "w3_beg", "w3_last", "ep_accfull", "ep_accempty", "ep_stored", "x"]
 for j in range(int(sys.argv[3]) if len(sys.argv) > 3 else 0, (int(sys.argv[3]) if len(sys.argv) > 3 else 0) + 24):
     row = [(t[e, j] - t0) if t[e, j] > 0 else -1 for e in range(8)]
     print(j, " ".join(f"{n}={v:8d}" for n, v in zip(names, row)))
