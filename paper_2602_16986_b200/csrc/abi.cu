@@ -367,8 +367,10 @@ uh_status uh_layer_bwd(const uh_jagged* jag, uh_mask m, const uh_layer_params* p
     gw2.M = d; gw2.N = d; gw2.K = (int)T;
     gw2.A = ybuf; gw2.lda = d; gw2.a_mn = true; gw2.B = dout; gw2.ldb = d; gw2.b_mn = true;
     gw2.epi = EPI_F32; gw2.out0 = grads->w2; gw2.ld0 = d;
+    const bool fuse_cs = dtype == UH_BF16 && d % 256 == 0;   // db2 / db1 from the dW GEMMs' staged B tiles
+    if (p->b2 && fuse_cs) gw2.colsum = grads->b2;
     UH_TRY(gemm_run(gw2, dtype, st));
-    if (p->b2) UH_TRY(colsum(dtype, T, d, dout, d, grads->b2, st));
+    if (p->b2 && !fuse_cs) UH_TRY(colsum(dtype, T, d, dout, d, grads->b2, st));
     // B4: attention backward -> dH[:, V|Q|K] (x silu'(h)), d rab
     AttnCall c{};
     c.jag = jag; c.mask = m; c.desc = &p->attn;
@@ -385,8 +387,9 @@ uh_status uh_layer_bwd(const uh_jagged* jag, uh_mask m, const uh_layer_params* p
     gw1.M = d; gw1.N = 4 * d; gw1.K = (int)T;
     gw1.A = xh; gw1.lda = d; gw1.a_mn = true; gw1.B = dH; gw1.ldb = 4 * d; gw1.b_mn = true;
     gw1.epi = EPI_F32; gw1.out0 = grads->w1; gw1.ld0 = 4 * d;
+    if (p->b1 && fuse_cs) gw1.colsum = grads->b1;
     UH_TRY(gemm_run(gw1, dtype, st));
-    if (p->b1) UH_TRY(colsum(dtype, T, 4 * d, dH, 4 * d, grads->b1, st));
+    if (p->b1 && !fuse_cs) UH_TRY(colsum(dtype, T, 4 * d, dH, 4 * d, grads->b1, st));
     GemmDesc gx;
     gx.M = (int)T; gx.N = d; gx.K = 4 * d;
     gx.A = dH; gx.lda = 4 * d; gx.B = p->w1; gx.ldb = 4 * d; gx.b_mn = false;

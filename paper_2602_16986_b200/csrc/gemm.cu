@@ -131,6 +131,7 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     a.k_splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
     a.out0 = g.out0; a.ld0 = g.ld0; a.out1 = g.out1; a.ld1 = g.ld1;
     a.bias = g.bias; a.resid = (const __nv_bfloat16*)g.resid; a.ldr = g.ldr;
+    a.colsum = (EPI == EPI_F32 && BMN && BN == 256) ? g.colsum : nullptr;
     const int total = a.m_tiles * a.n_tiles * a.k_splits;
     auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI, MSUB>;
     UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
@@ -150,6 +151,7 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
     if (g.epi == EPI_F32) {
         // weight gradients (K = tokens): 256 x 256 tiles (two 128-row sub-tiles share each B k-block)
         if (g.a_mn && g.b_mn && g.M % 256 == 0 && g.N % 256 == 0) return launch_sm100<256, true, true, EPI_F32, 2>(g, st);
+        if (g.colsum) return fail(UH_ERR_UNSUPPORTED, "fused column sums need the 256-wide split-K path");
         if (g.a_mn && g.b_mn) UH_G(128, true, true, EPI_F32);
         if (!g.a_mn && !g.b_mn) UH_G(128, false, false, EPI_F32);
         return fail(UH_ERR_UNSUPPORTED, "gemm EPI_F32 with mixed majors");

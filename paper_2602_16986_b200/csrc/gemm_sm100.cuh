@@ -31,6 +31,7 @@ struct GemmArgs {
     void* out1; int64_t ld1;
     const float* bias;
     const __nv_bfloat16* resid; int64_t ldr;
+    float* colsum;      // EPI_F32, 256-wide MN-major B: += column sums of B (the bias gradient), or null
 };
 
 // MSUB row sub-tiles of 128 share each B k-block (tile BM = 128 MSUB): for the long-K split-K
@@ -44,7 +45,8 @@ struct GemmCfg {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGING = EPI == 2 ? 0 : 8 * 2 * 2048;   // per epilogue warp: a 32x32 bf16 box per output
+    // per epilogue warp a 32x32 bf16 box per output (TMA stores); EPI_F32: [8 row groups][BN] column-sum partials
+    static constexpr int STAGING = EPI == 2 ? 8 * BN * 4 : 8 * 2 * 2048;
     static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int NACC = 2 * MSUB * BN <= 512 ? 2 : 1;
     static constexpr int TMEM_COLS = NACC * MSUB * BN <= 256 ? 256 : 512;
@@ -70,7 +72,9 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int total = g.m_tiles * g.n_tiles * g.k_splits;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        // with fused column sums the 8 epilogue warps also read every B stage before it is released
+        const int cs_arrivals = (EPI == EPI_F32 && g.colsum) ? 8 : 0;
+        for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + cs_arrivals); }
         for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
         fence_barrier_init();
     }
@@ -168,9 +172,53 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int wg = (warp - 4) >> 2;       // column half of the tile
         const int row_in_tile = wq * 32 + (int)lane_id();
         int it = 0;
+        int cs_stage = 0; uint32_t cs_phase = 0;   // B-stage sequence (mirrors the MMA issuer's)
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
             int mt, nt, ks;
             decode(t, mt, nt, ks);
+            if (EPI == EPI_F32 && B_MN && BN == 256 && g.colsum) {
+                // bias gradient = column sums of B, read from the staged k-blocks (m-tile 0 only, so
+                // each B element is counted once): thread -> 8 columns x 8 rows of every stage
+                const int et = threadIdx.x - 128, c = et & 31, r = et >> 5;
+                float cs[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) cs[e] = 0.f;
+                int kb0, kb1;
+                kb_range(ks, kb0, kb1);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    mbar_wait(&full[cs_stage], cs_phase);
+                    if (mt == 0) {
+                        const uint8_t* b = sB + cs_stage * C::B_BYTES + (c >> 3) * (64 * C::BK * 2);
+#pragma unroll
+                        for (int rr = 0; rr < 8; ++rr) {
+                            const int k = r * 8 + rr;
+                            const uint4 u = *reinterpret_cast<const uint4*>(b + k * 128 + (((c & 7) ^ rr) << 4));
+                            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float2 f = unpack_bf16x2(w[q]);
+                                cs[2 * q] += f.x;
+                                cs[2 * q + 1] += f.y;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane_id() == 0) mbar_arrive(&empty[cs_stage]);
+                    if (++cs_stage == C::STAGES) { cs_stage = 0; cs_phase ^= 1; }
+                }
+                if (mt == 0) {
+                    float* red = reinterpret_cast<float*>(stg);   // [8 row groups][BN]
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) red[r * BN + c * 8 + e] = cs[e];
+                    named_bar_sync(1, 256);
+                    float sum = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) sum += red[q * BN + et];
+                    const int col = nt * BN + et;
+                    if (col < g.N && sum != 0.f) atomicAdd(g.colsum + col, sum);
+                    named_bar_sync(1, 256);
+                }
+            }
             const int acc = C::NACC == 2 ? (it & 1) : 0;
             mbar_wait(&tfull[acc], C::NACC == 2 ? ((it >> 1) & 1) : (it & 1));
             tc_fence_after();

@@ -45,6 +45,7 @@ struct GemmDesc {
     void* out1 = nullptr; int64_t ld1 = 0;
     const float* bias = nullptr;
     const void* resid = nullptr; int64_t ldr = 0;
+    float* colsum = nullptr;   // EPI_F32 only: += column sums of B (fused bias gradient)
 };
 uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st);
 
