@@ -140,8 +140,33 @@ def run_ours(args, rank, world, local_rank):
     ws_f = U._ws(U.layer_workspace_bytes(jag, m, prm, attn, U.BF16, False), device)
     ws_b = U._ws(U.layer_workspace_bytes(jag, m, prm, attn, U.BF16, True), device)
 
+    def layer_fb(xx, dd, at):   # the layer's forward + rematerialising backward (grads into the bucket)
+        U.layer_fwd(jag, m, prm, at, xx, out=out, ws=ws_f, saved=saved)
+        U.layer_bwd(jag, m, prm, at, xx, saved, dd, grads=bucket.views, dx=dx, ws=ws_b)
+
+    # The layer's ~20 launches are stream-ordered with no host synchronisation (F0 runs on the
+    # device), so the forward + backward is captured once as a CUDA graph and replayed; the
+    # gradient all-reduce stays outside the graph (NCCL, every N the same path).
+    graph, graph_launches = None, 0
+    if not args.no_graph:
+        cs0 = torch.cuda.Stream(device)
+        cs0.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs0):
+            layer_fb(x, dout, attn)
+        torch.cuda.current_stream().wait_stream(cs0)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        lc0 = U.launch_count()
+        with torch.cuda.graph(graph):
+            layer_fb(x, dout, attn)
+        graph_launches = U.launch_count() - lc0   # kernels recorded into the graph (one replay = one step)
+
     def step(xx, dd):   # one DP training step of the layer on this rank's shard (+ grad all-reduce)
-        D.layer_step(jag, m, prm, attn, xx, dd, bucket, saved=saved, out=out, dx=dx, ws_f=ws_f, ws_b=ws_b)
+        if graph is not None and xx is x and dd is dout:
+            graph.replay()
+        else:
+            layer_fb(xx, dd, attn)
+        bucket.allreduce_()
 
     def barrier():
         if world > 1:
@@ -170,7 +195,7 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank) if rank == 0 else None
     l0 = U.launch_count()
     ms = timed(lambda: step(x, dout), args.steps)
-    launches = U.launch_count() - l0
+    launches = U.launch_count() - l0 + (graph_launches * args.steps if graph is not None else 0)
     ms_step = ms / args.steps
     total_tokens = T * world if cfg.name == "cfg3" else sum(cfg.lengths)
     value = total_tokens / (ms_step / 1e3)
@@ -259,7 +284,8 @@ def run_ours(args, rank, world, local_rank):
                                f"{cfg.K2} global, rab (P={cfg.P}, NB={cfg.ts_len}), N={int(cfg.N)}",
                    "global_batch_tokens": total_tokens, "seq_len": max(W["lengths"]),
                    "parallelism": f"dp{world} (LPT token-balanced shards, NCCL all-reduce of the fp32 grad bucket)",
-                   "l2": "inputs larger than L2 (x 268 MB, step working set ~8 GB)"},
+                   "l2": "inputs larger than L2 (x 268 MB, step working set ~8 GB)",
+                   "launch": "CUDA graph replay of the layer fwd+bwd" if graph is not None else "eager launches"},
         "attn": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "nnz_pairs_per_head": nnz,
                  "effective_tflops": attn_tflops, "fwd_tflops": fwd_flop / (fwd_ms / 1e3) / 1e12,
                  "bwd_tflops": bwd_flop / (bwd_ms / 1e3) / 1e12,
@@ -359,6 +385,7 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:
