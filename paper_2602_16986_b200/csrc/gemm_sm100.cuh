@@ -219,6 +219,15 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     named_bar_sync(1, 256);
                 }
             }
+            // this warp's bias columns, one per lane per 32-column chunk, loaded before the
+            // accumulator wait (their latency hides behind the main loop); broadcast by shuffles
+            constexpr int NCH = BN / 64;   // 32-column chunks per warpgroup half
+            float bl[NCH];
+#pragma unroll
+            for (int q = 0; q < NCH; ++q) {
+                const int cb = nt * BN + wg * (BN / 2) + 32 * q + (int)lane_id();
+                bl[q] = (EPI != EPI_F32 && g.bias && cb < g.N) ? __ldg(g.bias + cb) * (EPI == EPI_SILU ? 0.5f : 1.0f) : 0.f;
+            }
             const int acc = C::NACC == 2 ? (it & 1) : 0;
             mbar_wait(&tfull[acc], C::NACC == 2 ? ((it >> 1) & 1) : (it & 1));
             tc_fence_after();
@@ -242,17 +251,13 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 } else {
                     // h = acc + bias (EPI_SILU: h/2 carried, silu(2h') = h' + h' tanh h'); packed bf16
                     float hb[32];
-                    const float bsc = EPI == EPI_SILU ? 0.5f : 1.0f;
-                    if (g.bias && col + 32 <= g.N) {
-                        const float4* bp = reinterpret_cast<const float4*>(g.bias + col);
+                    {
+                        const int q = (c0 - wg * (BN / 2)) >> 5;   // chunk index within the half
+                        float bq = bl[0];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 b4 = __ldg(bp + j);
-                            hb[4 * j] = b4.x * bsc; hb[4 * j + 1] = b4.y * bsc; hb[4 * j + 2] = b4.z * bsc; hb[4 * j + 3] = b4.w * bsc;
-                        }
-                    } else {
+                        for (int qq = 1; qq < NCH; ++qq) bq = q == qq ? bl[qq] : bq;
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) hb[j] = (g.bias && col + j < g.N) ? __ldg(g.bias + col + j) * bsc : 0.f;
+                        for (int j = 0; j < 32; ++j) hb[j] = __shfl_sync(0xffffffffu, bq, j);
                     }
                     uint32_t o0[16], o1[16];
                     if (EPI == EPI_BF16) {
