@@ -147,6 +147,19 @@ def run_ours(args, rank, world, local_rank):
     # The layer's ~20 launches are stream-ordered with no host synchronisation (F0 runs on the
     # device), so the forward + backward is captured once as a CUDA graph and replayed; the
     # gradient all-reduce stays outside the graph (NCCL, every N the same path).
+    stack = None
+    if cfg.n_layers > 1:   # cfg4: the L-layer stack, per-layer buckets all-reduced as each backward ends
+        from paper_2602_16986_b200 import synth as _synth
+        layers = []
+        for li in range(cfg.n_layers):
+            pl = _synth.layer_params(d, cfg.seed, layer=li)
+            f = lambda a: torch.from_numpy(a).to(device)
+            bb = lambda a: torch.from_numpy(a).to(device, torch.bfloat16)
+            layers.append((U.Params(f(pl["ln1_w"]), f(pl["ln1_b"]), bb(pl["w1"]), f(pl["ln2_w"]), f(pl["ln2_b"]),
+                                    bb(pl["w2"]), f(pl["b1"]), f(pl["b2"])), attn))
+        stack = D.Stack(jag, m, layers, x)
+        args.no_graph = True
+        args.no_e2e = True
     graph, graph_launches = None, 0
     if not args.no_graph:
         cs0 = torch.cuda.Stream(device)
@@ -162,6 +175,11 @@ def run_ours(args, rank, world, local_rank):
         graph_launches = U.launch_count() - lc0   # kernels recorded into the graph (one replay = one step)
 
     def step(xx, dd):   # one DP training step of the layer on this rank's shard (+ grad all-reduce)
+        if stack is not None:
+            _, _, hs = stack.step(xx, dd)
+            for hd in hs:
+                hd.wait()
+            return
         if graph is not None and xx is x and dd is dout:
             graph.replay()
         else:
@@ -279,9 +297,13 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: ULTRA-HSTU layer fwd+bwd, {len(W['lengths'])} jagged seqs x L="
-                               f"{max(W['lengths'])} per GPU ({T} tokens), 4 heads x 128, SLA window {cfg.K1} + "
-                               f"{cfg.K2} global, rab (P={cfg.P}, NB={cfg.ts_len}), N={int(cfg.N)}",
+        "config": {"workload": (f"{cfg.name}: ULTRA-HSTU layer fwd+bwd, {len(W['lengths'])} jagged seqs x L="
+                                f"{max(W['lengths'])} per GPU ({T} tokens), 4 heads x 128, SLA window {cfg.K1} + "
+                                f"{cfg.K2} global, rab (P={cfg.P}, NB={cfg.ts_len}), N={int(cfg.N)}")
+                               if cfg.n_layers == 1 else
+                               (f"{cfg.name}: {cfg.n_layers}-layer ULTRA-HSTU stack fwd+bwd, {len(W['lengths'])} jagged "
+                                f"seqs (log-uniform 512..16384) = {T} tokens on rank 0, 4 heads x 128, SLA {cfg.K1} + "
+                                f"{cfg.K2} global, rab, per-layer grad buckets all-reduced as each backward ends"),
                    "global_batch_tokens": total_tokens, "seq_len": max(W["lengths"]),
                    "parallelism": f"dp{world} (LPT token-balanced shards, NCCL all-reduce of the fp32 grad bucket)",
                    "l2": "inputs larger than L2 (x 268 MB, step working set ~8 GB)",

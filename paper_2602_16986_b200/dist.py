@@ -71,3 +71,41 @@ def layer_step(jag: U.JaggedBatch, m: U.Mask, prm: U.Params, attn: U.Attn, x: to
     dx, _ = U.layer_bwd(jag, m, prm, attn, x, saved, dout, grads=bucket.views, dx=dx, ws=ws_b)
     bucket.allreduce_(group)
     return out, dx
+
+
+class Stack:
+    """An L-layer HSTU stack on one rank's shard with every buffer pre-allocated: per layer the
+    remat saved set, the layer output and a flat fp32 gradient bucket (one
+    bucket per layer, all-reduced as soon as that layer's backward has finished)."""
+
+    def __init__(self, jag: U.JaggedBatch, m: U.Mask, layers: Sequence[Tuple[U.Params, U.Attn]], x: torch.Tensor):
+        self.jag, self.m, self.layers = jag, m, list(layers)
+        self.saved = [U.alloc_saved(x) for _ in self.layers]
+        self.h = [torch.empty_like(x) for _ in self.layers]          # layer outputs
+        self.g = [torch.empty_like(x), torch.empty_like(x)]          # ping-pong input gradients
+        self.buckets = [GradBucket.for_layer(p, a, x.device) for p, a in self.layers]
+        prm0, att0 = self.layers[0]
+        self.ws_f = U._ws(U.layer_workspace_bytes(jag, m, prm0, att0, U.BF16, False), x.device)
+        self.ws_b = U._ws(U.layer_workspace_bytes(jag, m, prm0, att0, U.BF16, True), x.device)
+
+    def step(self, x: torch.Tensor, dout: torch.Tensor, group=None):
+        """Forward through every layer, then the backward in reverse; layer l's gradient bucket
+        is all-reduced asynchronously right after its backward (NCCL overlaps layer l-1's
+        backward).  Returns the output, dx and the pending all-reduce handles."""
+        h = x
+        for (prm, attn), sv, out in zip(self.layers, self.saved, self.h):
+            U.layer_fwd(self.jag, self.m, prm, attn, h, out=out, ws=self.ws_f, saved=sv)
+            h = out
+        handles = []
+        g = dout
+        for l in range(len(self.layers) - 1, -1, -1):
+            prm, attn = self.layers[l]
+            inp = x if l == 0 else self.h[l - 1]
+            dx = self.g[l & 1]
+            U.layer_bwd(self.jag, self.m, prm, attn, inp, self.saved[l], g, grads=self.buckets[l].views, dx=dx,
+                        ws=self.ws_b)
+            hd = self.buckets[l].allreduce_(group, async_op=True)
+            if hd is not None:
+                handles.append(hd)
+            g = dx
+        return h, g, handles
