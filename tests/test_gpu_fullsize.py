@@ -85,3 +85,36 @@ def test_layer_cfg3_full_size_sampled_sequence():
     assert rel_inf(to_np(out[rows]), ref_out) <= TOL
     ref_dx, _ = O.layer_backward(dout[rows], one, prm_o, cfg.H, spec, cache=cache)
     assert rel_inf(to_np(dx[rows]), ref_dx) <= TOL
+
+
+def test_attention_cfg2_full_size_sampled_sequences():
+    """cfg2 (BASELINE configs[1]): 32 sequences of U[1024, 4096] tokens, full causal, rab on."""
+    cfg = synth.config("cfg2")
+    off = cfg.offsets()
+    q, k, v, dA = synth.attn_inputs(cfg)
+    pos, ts = synth.rab_tables(cfg)
+    t = synth.timestamps(cfg.seed, cfg.lengths)
+    d = cfg.d
+    buf = torch.empty(cfg.T, 4 * d, dtype=torch.bfloat16, device="cuda")
+    buf[:, d:2 * d] = to_dev(v, U.BF16)
+    buf[:, 2 * d:3 * d] = to_dev(q, U.BF16)
+    buf[:, 3 * d:] = to_dev(k, U.BF16)
+    jag = U.JaggedBatch(off)
+    attn = U.Attn(cfg.H, cfg.dh, cfg.alpha, float(cfg.N), torch.from_numpy(pos).cuda(), torch.from_numpy(ts).cuda(),
+                  torch.from_numpy(t).cuda())
+    m = U.mask(cfg.K1, cfg.K2)
+    Q, K, V = buf[:, 2 * d:3 * d], buf[:, 3 * d:], buf[:, d:2 * d]
+    A = U.attn_fwd(jag, m, attn, Q, K, V)
+    dq, dk, dv, _, _ = U.attn_bwd(jag, m, attn, Q, K, V, to_dev(dA, U.BF16))
+    torch.cuda.synchronize()
+    longest = int(np.argmax(cfg.lengths))
+    for b in sorted({longest, 5}):
+        r0, r1 = int(off[b]), int(off[b + 1])
+        rows = slice(r0, r1)
+        one = np.array([0, r1 - r0], np.int32)
+        spec = O.AttnSpec(K1=O.FULL, K2=0, alpha=cfg.alpha, N=float(cfg.N), pos_w=pos, ts_w=ts, timestamps=t[rows])
+        assert rel_inf(to_np(A[rows]), O.attention_forward(one, cfg.H, cfg.dh, q[rows], k[rows], v[rows], spec)) <= TOL
+        ref = O.attention_backward(one, cfg.H, cfg.dh, q[rows], k[rows], v[rows], dA[rows], spec)
+        for name, got, r in zip(("dQ", "dK", "dV"), (dq, dk, dv), ref[:3]):
+            e = rel_inf(to_np(got[rows]), r)
+            assert e <= TOL, (b, name, e)

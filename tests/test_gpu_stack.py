@@ -60,3 +60,56 @@ def test_truncated_inference_stack(l_keep):
         spec = O.AttnSpec(K1=O.FULL, K2=0, alpha=1.0, N=float(l_keep), pos_w=pos, ts_w=ts, timestamps=t2)
         h, _ = O.layer_forward(h, off2, prm, H, spec)
     assert rel_inf(to_np(out), h) <= 2e-2
+
+
+def test_cfg4_like_stack_per_layer_against_oracle():
+    """cfg4's shape at test size: log-uniform (long-tail) lengths through a 3-layer stack with
+    independent weights.  Every layer is checked against the oracle given the GPU's own input
+    and incoming gradient (teacher forcing); Stack.step reproduces the chain."""
+    from paper_2602_16986_b200 import dist as D
+    lengths = synth.lengths_loguniform_until(4, 32, 1500, 6000)
+    H, dh, n_layers = 2, 128, 3
+    d = H * dh
+    cfg = synth.Config("stack4", lengths, H=H, dh=dh, K1=256, K2=32, N=1500.0, seed=4, pos_len=64)
+    x, dout = synth.layer_inputs(cfg)
+    pos, ts = synth.rab_tables(cfg)
+    t = synth.timestamps(cfg.seed, lengths)
+    f = lambda a: torch.from_numpy(a).cuda()
+    w = lambda a: torch.from_numpy(a).to("cuda", torch.bfloat16)
+    attn = U.Attn(H, dh, 1.0, cfg.N, f(pos), f(ts), f(t))
+    m = U.mask(cfg.K1, cfg.K2)
+    jag = U.JaggedBatch(cfg.offsets())
+    params = [synth.layer_params(d, cfg.seed, layer=l) for l in range(n_layers)]
+    prms = [U.Params(f(p["ln1_w"]), f(p["ln1_b"]), w(p["w1"]), f(p["ln2_w"]), f(p["ln2_b"]), w(p["w2"]),
+                     f(p["b1"]), f(p["b2"])) for p in params]
+    X, G = to_dev(x, U.BF16), to_dev(dout, U.BF16)
+    # the chain, layer by layer through the C ABI
+    hs, saved = [X], []
+    for prm in prms:
+        out, sv = U.layer_fwd(jag, m, prm, attn, hs[-1])
+        hs.append(out)
+        saved.append(sv)
+    gs, grads = [None] * n_layers, [None] * n_layers
+    g = G
+    for l in range(n_layers - 1, -1, -1):
+        dx, gr = U.layer_bwd(jag, m, prms[l], attn, hs[l], saved[l], g)
+        gs[l], grads[l] = g, gr
+        g = dx
+    torch.cuda.synchronize()
+    off = cfg.offsets()
+    spec = O.AttnSpec(K1=cfg.K1, K2=cfg.K2, alpha=1.0, N=cfg.N, pos_w=pos, ts_w=ts, timestamps=t)
+    for l in range(n_layers):
+        prm_o = O.LayerParams(**{k: np.asarray(v, np.float64) for k, v in params[l].items()})
+        ref_out, cache = O.layer_forward(to_np(hs[l]), off, prm_o, H, spec)
+        assert rel_inf(to_np(hs[l + 1]), ref_out) <= 2e-2, ("out", l)
+        ref_dx, ref_g = O.layer_backward(to_np(gs[l]), off, prm_o, H, spec, cache=cache)
+        dx_l = gs[l - 1] if l > 0 else g        # layer l's dx is layer l-1's incoming gradient
+        assert rel_inf(to_np(dx_l), ref_dx) <= 2e-2, ("dx", l)
+        for k in ("w1", "w2", "ln1_w", "ln2_w", "b1"):
+            e = rel_inf(to_np(grads[l][k]), ref_g[k])
+            assert e <= 2e-2, (l, k, e)
+    # Stack.step runs the same calls in the same order: identical outputs and final dx
+    st = D.Stack(jag, m, list(zip(prms, [attn] * n_layers)), X)
+    out_s, dx_s, _ = st.step(X, G)
+    torch.cuda.synchronize()
+    assert torch.equal(out_s, hs[-1]) and torch.equal(dx_s, g)
