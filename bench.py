@@ -344,6 +344,83 @@ def roofline_bwd(bwd_flop: float, bwd_ms: float, peaks: dict, workload: str):
                             "algorithmic minimum ~1.6e9 (read Q, K, V, dA; write dQ, dK, dV)"}
 
 
+# ----------------------------------------------------------------------------- cfg5: inference
+def run_inference(args, rank, world, local_rank):
+    """cfg5 / NEXT-1: forward-only 18-layer stack with attention truncation —
+    6 SLA layers (window 1024 + 128 global) on the full sequences, then the latest 1024 tokens of
+    each sequence through 12 full-causal layers (stack.forward_truncated).  Replicas only: every
+    GPU runs its own batch, no collective.  value = input tokens of all GPUs per second."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_16986_b200 import stack as S
+    from paper_2602_16986_b200 import synth
+    from paper_2602_16986_b200 import uhstu as U
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    L, l_keep, n_sla, n_at = args.seq_len, 1024, 6, 12
+    B = max(1, args.tokens // L)
+    cfg = synth.Config("cfg5", [L] * B, H=4, dh=128, K1=1024, K2=128, N=L, seed=5 + rank, pos_len=128)
+    d = cfg.d
+    x = torch.from_numpy(synth.rows_normal(cfg.seed, cfg.lengths, d, 1.0, 0x61)).to(device, torch.bfloat16)
+    pos, ts = synth.rab_tables(cfg)
+    t = torch.from_numpy(synth.timestamps(cfg.seed, cfg.lengths)).to(device)
+    f = lambda a: torch.from_numpy(a).to(device)
+    bb = lambda a: torch.from_numpy(a).to(device, torch.bfloat16)
+    layers = []
+    for li in range(n_sla + n_at):
+        pl = synth.layer_params(d, cfg.seed, layer=li)
+        prm = U.Params(f(pl["ln1_w"]), f(pl["ln1_b"]), bb(pl["w1"]), f(pl["ln2_w"]), f(pl["ln2_b"]), bb(pl["w2"]),
+                       f(pl["b1"]), f(pl["b2"]))
+        attn = U.Attn(cfg.H, cfg.dh, 1.0, float(L), f(pos), f(ts), t)
+        m = U.mask(cfg.K1, cfg.K2) if li < n_sla else U.mask()
+        layers.append(S.Layer(prm, attn, m))
+    jag = U.JaggedBatch(cfg.offsets(), device)
+
+    def step():
+        S.forward_truncated(jag, x, layers, n_sla, l_keep, norm_n_truncated=float(l_keep))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    l0 = U.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    launches = U.launch_count() - l0
+    clocks = sampler.stop() if sampler else None
+    if rank != 0:
+        return None
+    ms_step = ms / args.steps
+    tokens = B * L * world
+    return {"metric": "HSTU inference tokens/s (cfg5: 6 SLA layers + truncation to 1024 + 12 full-causal layers)",
+            "value": tokens / (ms_step / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"cfg5: {B} sequences x L={L} per GPU ({B * L} tokens), 4 heads x 128, "
+                                   f"{n_sla} SLA layers (1024 + 128 global), latest {l_keep} tokens, {n_at} causal layers",
+                       "parallelism": f"replicas x{world} (no collective)", "seq_len": L},
+            "gpu_launches": launches, "clocks": clocks,
+            "e2e": None, "e2e_note": "inference inputs (x) stay resident; not measured for cfg5"}
+
+
 # ----------------------------------------------------------------------------- oracle arm
 def oracle_sample(cfg, L: int):
     """The oracle (as it stands) on one length-L sequence of the workload: layer fwd+bwd."""
@@ -404,7 +481,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--seq-len", type=int, default=16384, help="cfg5: sequence length (4096, 16384, 65536)")
+    ap.add_argument("--tokens", type=int, default=4 * 1048576, help="cfg5: tokens per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
@@ -423,7 +502,7 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        line = run_ours(args, rank, world, local_rank)
+        line = (run_inference if args.config == "cfg5" else run_ours)(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
