@@ -1,0 +1,21 @@
+"""Timeline of CTA 0 of the forward kernel (trace build): per tile, when the MMA warp got
+K/V, when it got P, and when epilogue warp 4 waited for / got S and finished P."""
+import ctypes, os, sys
+import numpy as np, torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2602_16986_b200 import uhstu as U
+U.LIB_PATH = os.path.join(ROOT, "paper_2602_16986_b200", "lib", "libuhstu_trace.so")
+L = U.lib()
+buf = torch.zeros(8192, dtype=torch.int64, device="cuda")
+L.uh_trace_set.argtypes = [ctypes.c_void_p]
+print("set", L.uh_trace_set(ctypes.c_void_p(buf.data_ptr())))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from attn_time import run
+run(B=16, rab=bool(int(sys.argv[1])) if len(sys.argv) > 1 else False, steps=1)
+t = buf.view(8, 1024).cpu().numpy()
+t0 = t[t > 0].min()
+names = ["c0_ldbeg", "c0_ldok", "wait_s", "got_s", "computed", "arrived", "c1_ldbeg", "c1_ldok"]
+for j in range(400, 416):
+    row = [(t[e, j] - t0) if t[e, j] > 0 else -1 for e in range(8)]
+    print(j, " ".join(f"{n}={v:8d}" for n, v in zip(names, row)))
