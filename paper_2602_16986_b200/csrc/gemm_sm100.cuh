@@ -141,9 +141,14 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             mbar_wait(&tempty[acc], (C::NACC == 2 ? ((it >> 1) & 1) : (it & 1)) ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * MSUB * BN;
+            // the next k-block's stage is probed (test_wait, never parks) before this block's MMAs
+            // are issued and waited on after them: a blocking wait between blocks drains the MMA queue
+            mbar_wait(&full[stage], phase);
             for (int kb = kb0; kb < kb1; ++kb) {
-                mbar_wait(&full[stage], phase);
                 tc_fence_after();
+                const int nst = stage + 1 == C::STAGES ? 0 : stage + 1;
+                const uint32_t nph = stage + 1 == C::STAGES ? phase ^ 1 : phase;
+                const bool rdy = mbar_test(smem_u32(&full[nst]), nph);
                 if (elect_one()) {
                     const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
                     const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
@@ -161,7 +166,8 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     umma_commit(&empty[stage]);
                 }
                 __syncwarp();
-                if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                stage = nst; phase = nph;
+                if (kb + 1 < kb1 && !rdy) mbar_wait(&full[stage], phase);
             }
             if (elect_one()) umma_commit(&tfull[acc]);
             __syncwarp();
