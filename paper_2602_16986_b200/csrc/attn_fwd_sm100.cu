@@ -253,9 +253,10 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     if (ch.flags & FLAG_M) apply_vis(hx, q_vis_bits(cx, qp, qok, kb));   // h = 0 -> P = 0
                     uint32_t pk[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
-                        pk[i] = fma_bf16x2(h2, tanh_bf16x2(h2), h2);
+                    for (int i = 0; i < 16; ++i) {   // fp32 tanh, h + h t as one packed FFMA2, one bf16 pack
+                        const uint64_t H = f2_pack(hx[2 * i], hx[2 * i + 1]);
+                        const float2 p2 = f2_unpack(ffma2(H, f2_pack(tanh_approx(hx[2 * i]), tanh_approx(hx[2 * i + 1])), H));
+                        pk[i] = pack_bf16(p2.x, p2.y);
                     }
                     // P -> TMEM over the chunk's own (already read) S columns: keys [32hc, 32hc+32) at col 32hc
                     tmem_st16(tmem + lane_base + sb * BN + 32 * hc, pk);
