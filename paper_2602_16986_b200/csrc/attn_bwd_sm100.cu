@@ -326,13 +326,14 @@ attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     float hx[32];
                     q_h<false>(cx, ch, tq, sv, hx, nullptr);
                     if (ch.flags & FLAG_M) apply_vis(dp, q_vis_bits(cx, qp, qok, kb));   // dP = 0 -> dS = 0
+                    const uint64_t one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const uint32_t h2 = pack_bf16(hx[2 * i], hx[2 * i + 1]);
-                        const uint32_t t2 = tanh_bf16x2(h2);
-                        const uint32_t a1 = add_bf16x2(t2, kBf16One2);
-                        const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
-                        d2[i] = mul_bf16x2(pack_bf16(dp[2 * i], dp[2 * i + 1]), mul_bf16x2(a1, wv));
+                    for (int i = 0; i < 16; ++i) {   // fp32 pairs: (1 + t)(1 + h (1 - t)) dP, one bf16 pack
+                        const uint64_t H = f2_pack(hx[2 * i], hx[2 * i + 1]);
+                        const uint64_t T = f2_pack(tanh_approx(hx[2 * i]), tanh_approx(hx[2 * i + 1]));
+                        const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
+                        const float2 v = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * i], dp[2 * i + 1]), fadd2(T, one2)), W));
+                        d2[i] = pack_bf16(v.x, v.y);
                     }
                 }
                 if (!qok) {
@@ -638,14 +639,17 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     apply_vis(dp, m);
                 }
                 uint32_t p2[16], d2[16];
+                const uint64_t one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const uint32_t h2 = pack_bf16(hx[2 * c], hx[2 * c + 1]);
-                    const uint32_t t2 = tanh_bf16x2(h2);
-                    const uint32_t a1 = add_bf16x2(t2, kBf16One2);
-                    p2[c] = mul_bf16x2(h2, a1);
-                    const uint32_t wv = fma_bf16x2(h2, fma_bf16x2(t2, kBf16NegOne2, kBf16One2), kBf16One2);
-                    d2[c] = mul_bf16x2(pack_bf16(dp[2 * c], dp[2 * c + 1]), mul_bf16x2(a1, wv));
+                for (int c = 0; c < 16; ++c) {   // fp32 pairs: P = h (1 + t), dS = dP (1 + t)(1 + h (1 - t))
+                    const uint64_t H = f2_pack(hx[2 * c], hx[2 * c + 1]);
+                    const uint64_t T = f2_pack(tanh_approx(hx[2 * c]), tanh_approx(hx[2 * c + 1]));
+                    const uint64_t A1 = fadd2(T, one2);
+                    const float2 pv = f2_unpack(fmul2(H, A1));
+                    p2[c] = pack_bf16(pv.x, pv.y);
+                    const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
+                    const float2 dv = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * c], dp[2 * c + 1]), A1), W));
+                    d2[c] = pack_bf16(dv.x, dv.y);
                 }
                 // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
                 tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);
