@@ -308,9 +308,13 @@ UH_DEV void k_h(const ChunkCtx& c, const Chunk& ch, int32_t tk, const float* s, 
     if (ch.flags & FLAG_T1) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, j >= ch.n ? ch.hbias_o : ch.hbias);
-    } else {
+    } else {   // common chunk: one packed FFMA2 per pair
+        const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, ch.hbias);
+        for (int j = 0; j < 32; j += 2) {
+            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, B2));
+            h[j] = v.x; h[j + 1] = v.y;
+        }
     }
     if (ch.flags & FLAG_P) {
         const float* pe = c.pos_e + kPosPad + ch.bd;

@@ -285,15 +285,19 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         }
 #pragma unroll
                         for (int i = 0; i < 16; ++i) o0[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-                    } else {  // EPI_SILU (fp32): silu = h + h t;  silu' = (1 + t)(1 + h (1 - t)) / 2;  h = acc/2, t = tanh h
+                    } else {  // EPI_SILU (packed fp32): silu = h + h t;  silu' = (1 + t)(1 + h (1 - t)) / 2;  h = acc/2, t = tanh h
+                        const uint64_t half2 = f2_pack(0.5f, 0.5f), one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            const float h0 = fmaf(v[2 * i], 0.5f, hb[2 * i]), h1 = fmaf(v[2 * i + 1], 0.5f, hb[2 * i + 1]);
-                            const float t0 = tanh_approx(h0), t1 = tanh_approx(h1);
-                            o0[i] = pack_bf16(fmaf(h0, t0, h0), fmaf(h1, t1, h1));
-                            if (g.out1)
-                                o1[i] = pack_bf16(fmaf(t0, 0.5f, 0.5f) * (fmaf(-h0, t0, h0) + 1.f),
-                                                  fmaf(t1, 0.5f, 0.5f) * (fmaf(-h1, t1, h1) + 1.f));
+                            const uint64_t H = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), half2, f2_pack(hb[2 * i], hb[2 * i + 1]));
+                            const float2 hh = f2_unpack(H);
+                            const uint64_t T = f2_pack(tanh_approx(hh.x), tanh_approx(hh.y));
+                            const float2 sv = f2_unpack(ffma2(H, T, H));
+                            o0[i] = pack_bf16(sv.x, sv.y);
+                            if (g.out1) {
+                                const float2 gv = f2_unpack(fmul2(ffma2(T, half2, half2), ffma2(H, ffma2(T, neg2, one2), one2)));
+                                o1[i] = pack_bf16(gv.x, gv.y);
+                            }
                         }
                     }
                     // rows of this warp -> its 64B-swizzled 32x32 staging boxes -> TMA stores
