@@ -123,9 +123,9 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     const int nkb = (g.K + C::BK - 1) / C::BK;
     const int sms = num_sms();
     int splits = 1;
-    if (EPI == EPI_F32) {
+    if (EPI == EPI_F32) {   // split-K: one wave (tiles x splits <= SMs; a partial second wave doubles the critical path)
         const int tiles = a.m_tiles * a.n_tiles;
-        splits = std::max(1, std::min(nkb, (sms + tiles - 1) / tiles));
+        splits = std::max(1, std::min(nkb, sms / std::max(1, tiles)));
     }
     a.kb_per_split = (nkb + splits - 1) / splits;
     a.k_splits = (nkb + a.kb_per_split - 1) / a.kb_per_split;
@@ -161,6 +161,12 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         if (wide) { if (g.b_mn) UH_G(256, false, true, EPI_SILU); UH_G(256, false, false, EPI_SILU); }
         if (g.b_mn) UH_G(128, false, true, EPI_SILU);
         UH_G(128, false, false, EPI_SILU);
+    }
+    // long K (dx^ = dH W1^T, K = 4d): 256 x 256 tiles of two 128-row sub-tiles halve the B ingress
+    // per flop; the single accumulator's unoverlapped epilogue is small against the K loop
+    if (wide && g.K >= 1024 && g.M % 256 == 0 && !g.resid) {
+        if (g.b_mn) return launch_sm100<256, false, true, EPI_BF16, 2>(g, st);
+        return launch_sm100<256, false, false, EPI_BF16, 2>(g, st);
     }
     if (wide) { if (g.b_mn) UH_G(256, false, true, EPI_BF16); UH_G(256, false, false, EPI_BF16); }
     if (g.b_mn) UH_G(128, false, true, EPI_BF16);

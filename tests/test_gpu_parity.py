@@ -21,7 +21,7 @@ RAGGED = [0, 1, 2, 17, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 
 # ----------------------------------------------------------------------------- GEMM (test hook)
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
-@pytest.mark.parametrize("MNK", [(256, 512, 128), (296, 256, 192), (128, 2048, 512)])
+@pytest.mark.parametrize("MNK", [(256, 512, 128), (296, 256, 192), (128, 2048, 512), (768, 512, 1024)])
 def test_gemm_bf16_majors(a_mn, b_mn, MNK):
     M, N, K = MNK
     g = torch.Generator().manual_seed(0)
