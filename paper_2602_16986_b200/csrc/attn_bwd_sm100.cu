@@ -19,6 +19,8 @@
 // "silu_backward") and written straight into their slices of dH (no
 // concat).
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "attn_common.cuh"
 #include "internal.h"
@@ -682,19 +684,525 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 }
 }  // namespace dkv
 
+// ============================================================================ fused kernel
+// One pass per 128-key tile computes dV, dK and the dQ partials of every visible 64-query
+// step: dQ^T = K^T dS^T (SS, M = dh, N = 64) lands in the TMEM columns of the consumed
+// S^T, is read by a fourth warpgroup and added into an fp32 [T, H dh] buffer with TMA
+// reductions (in L2: the schedule's consecutive key tiles keep the touched query rows
+// L2-resident).  S, P and dP are computed once instead of once per kernel.  The same
+// warpgroup reduces d pos_bias / d time_bias from the dS^T tile in shared memory.
+namespace fb {
+constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per step
+constexpr int KT = BM * DH * 2;           // K / V tile (32 KB: 2 x 16 KB blocks of [128 rows x 128 B])
+constexpr int QT = BN * DH * 2;           // Q / dA tile (16 KB: 2 x 8 KB blocks of [64 rows x 128 B])
+constexpr int STAGES = 2;                 // (Q, dA) ring
+constexpr int DS_BYTES = BM * BN * 2;     // dS^T [128 keys][64 queries] bf16, one SW128 block
+constexpr int STG_BYTES = BN * 32 * 4;    // per dQ warp: [64 queries][32 dh] fp32 box
+constexpr int TSL = 4 * 32 * 32 * 4;      // d time_bias partials [4 warps][32 buckets][32 lanes]
+constexpr int THREADS = 512;              // w0 TMA, w1 MMA (S/dP), w2 TMEM alloc, w3 MMA (dV/dK/dQ),
+                                          // w4-11 P/dS epilogue, w12-15 dQ + d rab
+constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+constexpr int SMEM_DATA = 2 * KT + STAGES * 2 * QT + 2 * DS_BYTES + 4 * STG_BYTES + TSL + kPosTab * 4 + 256 + 512;
+constexpr int SMEM = SMEM_DATA + 1024;
+static_assert(SMEM <= 232448, "fused bwd shared memory");
+
+struct __align__(8) Bars {
+    uint64_t kv_full, kv_empty;
+    uint64_t qa_full[STAGES], qa_empty[STAGES];
+    uint64_t s_full[2], p_full[2];
+    uint64_t dq_full[2];    // dQ^T(i) in the S columns of buffer i & 1
+    uint64_t s_free[2];     // ... read by the dQ warps: the next S^T may overwrite them
+    uint64_t ds_free[2];    // dS^T shared buffer read by the dQ MMA and the d rab reduction
+    uint64_t acc_full, acc_empty;
+    ItemRing ring;
+    uint32_t tmem;
+};
+
+__device__ __forceinline__ int n_qtiles(int k0, int L, int K1, int K2) {
+    const int qe = query_end(k0, BM, L, K1, K2);
+    return (qe + BN - 1) / BN - k0 / BN;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA,
+                     const __grid_constant__ CUtensorMap tmDQ, AttnArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;                                   // K 32 KB | V 32 KB
+    uint8_t* sV = smem + KT;
+    uint8_t* sQA = smem + 2 * KT;                         // [STAGES] x (Q 16 KB | dA 16 KB)
+    uint8_t* sDS = sQA + STAGES * 2 * QT;                 // [2] x dS^T
+    float* sDQ = reinterpret_cast<float*>(sDS + 2 * DS_BYTES);   // [4 warps] x [64][32] fp32
+    float* tsl = sDQ + 4 * STG_BYTES / 4;                 // [4 warps][32 buckets][32 lanes]
+    float* pos_s = tsl + TSL / 4;
+    float* ts_s = pos_s + kPosTab;
+    Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(&bars->kv_full, 1); mbar_init(&bars->kv_empty, 1);
+        for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->qa_full[i], 1); mbar_init(&bars->qa_empty[i], 1); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 8); mbar_init(&bars->dq_full[i], 1);
+            mbar_init(&bars->s_free[i], 4); mbar_init(&bars->ds_free[i], 4);
+        }
+        mbar_init(&bars->acc_full, 1); mbar_init(&bars->acc_empty, 8);
+        ring_init(&bars->ring, 14);  // MMA warps 1, 3 + 8 P/dS warps + 4 dQ warps
+        fence_barrier_init();
+    }
+    stage_rab(a, pos_s, ts_s);
+    for (int i = threadIdx.x; i < TSL / 4; i += THREADS) tsl[i] = 0.f;
+    if (warp == 2) tmem_alloc<512>(&bars->tmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars->tmem;
+
+    if (warp == 0) {
+        // ============================================================ producer
+        if (lane == 0) {
+            int qc = 0, ki = 0;
+            for (;; ++ki) {
+                const int w = ring_claim_publish(&bars->ring, ki, a.counter, a.n_items);
+                if (w < 0) break;
+                const WorkItem it = a.items[w];
+                const int k0 = it.tile * BM, h = it.head & 0xFFFF;
+                const int n = n_qtiles(k0, it.seq_len, a.K1, a.K2);
+                mbar_wait_sleep(&bars->kv_empty, (ki & 1) ^ 1);
+                mbar_arrive_expect_tx(&bars->kv_full, 2 * KT);
+                tma_load_2d(sK, &tmK, &bars->kv_full, h * DH, it.seq_start + k0);
+                tma_load_2d(sK + KT / 2, &tmK, &bars->kv_full, h * DH + 64, it.seq_start + k0);
+                tma_load_2d(sV, &tmV, &bars->kv_full, h * DH, it.seq_start + k0);
+                tma_load_2d(sV + KT / 2, &tmV, &bars->kv_full, h * DH + 64, it.seq_start + k0);
+                for (int i = 0; i < n; ++i) {
+                    const int row = it.seq_start + (k0 / BN + i) * BN;
+                    const int s = qc % STAGES;
+                    uint8_t* st = sQA + s * 2 * QT;
+                    mbar_wait_sleep(&bars->qa_empty[s], ((qc / STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bars->qa_full[s], 2 * QT);
+                    tma_load_2d(st, &tmQ, &bars->qa_full[s], h * DH, row);
+                    tma_load_2d(st + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
+                    tma_load_2d(st + QT, &tmdA, &bars->qa_full[s], h * DH, row);
+                    tma_load_2d(st + QT + QT / 2, &tmdA, &bars->qa_full[s], h * DH + 64, row);
+                    ++qc;
+                }
+            }
+        }
+    } else if (warp == 1 || warp == 3) {
+        // ============================================================ MMA issuers
+        // warp 1: S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T into buffer i & 1, once the dQ warps have
+        // read dQ^T(i - 2) from it.  warp 3: dV += P^T dA, dK += dS^T Q (TMEM A operands), then
+        // dQ^T(i) = K^T dS^T (both from shared memory) over the consumed S^T columns — issued
+        // after the dV MMA that reads P^T there (one warp, tensor-pipe order).
+        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [K|V] x [Q|dA]^T (both K-major)
+        constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // [P^T|dS^T](TMEM) x [dA|Q] (MN-major)
+        constexpr uint32_t idesc_q = make_idesc_bf16(DH, BN, true, true);     // K^T (MN-major) x dS^T (MN-major)
+        int ki = 0, sc = 0;
+        if (warp == 1) {
+            const uint64_t kv_k = make_sw128_desc(smem_u32(sK), 16, 1024);       // K / V K-major (A)
+            const uint64_t q_k = make_sw128_desc(smem_u32(sQA), 16, 1024);       // Q / dA K-major (B)
+            int st_s = 0, ph_s = 0;
+            for (;; ++ki) {
+                const int w = ring_take(&bars->ring, ki, lane);
+                if (w < 0) break;
+                const WorkItem it = a.items[w];
+                const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+                const uint64_t dk = kv_k, dv = dk + (KT >> 4);
+                mbar_wait(&bars->kv_full, ki & 1);
+                mbar_wait(&bars->qa_full[st_s], ph_s);
+                mbar_wait(&bars->s_free[sc & 1], ((sc >> 1) - 1) & 1);   // (first steps: parity 1 of a fresh barrier passes)
+                for (int i = 0; i < n; ++i, ++sc) {
+                    const int sb = sc & 1;
+                    tc_fence_after();
+                    const int nst = st_s + 1 == STAGES ? 0 : st_s + 1, nph = st_s + 1 == STAGES ? ph_s ^ 1 : ph_s;
+                    const uint32_t qa_a = smem_u32(&bars->qa_full[nst]), sf_a = smem_u32(&bars->s_free[sb ^ 1]);
+                    const uint32_t sf_p = (((sc + 1) >> 1) - 1) & 1;
+                    const bool r1 = mbar_test(qa_a, nph), r2 = mbar_test(sf_a, sf_p);
+                    const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
+                    const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < DH / 16; ++kk) {
+                            const uint32_t oa = ((kk >> 2) * (KT / 2) + (kk & 3) * 32) >> 4;
+                            const uint32_t ob = ((kk >> 2) * (QT / 2) + (kk & 3) * 32) >> 4;
+                            umma_ss(d_s, dk + oa, dq + ob, idesc_s, kk > 0 ? 1u : 0u);
+                            umma_ss(d_p, dv + oa, dda + ob, idesc_s, kk > 0 ? 1u : 0u);
+                        }
+                        umma_commit(&bars->s_full[sb]);
+                    }
+                    __syncwarp();
+                    st_s = nst; ph_s = nph;
+                    if (i + 1 < n) {
+                        if (!r1) mbar_wait_addr(qa_a, nph);
+                        if (!r2) mbar_wait_addr(sf_a, sf_p);
+                    }
+                }
+            }
+        } else {
+            const uint64_t q_mn = make_sw128_desc(smem_u32(sQA), QT / 2, 1024);  // Q / dA MN-major (B)
+            const uint64_t kt_mn = make_sw128_desc(smem_u32(sK), KT / 2, 1024);  // K^T: M = dh over 2 blocks
+            const uint64_t ds_mn = make_sw128_desc(smem_u32(sDS), DS_BYTES, 1024);  // dS^T: N = 64 queries
+            int st_a = 0;
+            for (;; ++ki) {
+                const int w = ring_take(&bars->ring, ki, lane);
+                if (w < 0) break;
+                const WorkItem it = a.items[w];
+                const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
+                mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
+                mbar_wait(&bars->p_full[sc & 1], (sc >> 1) & 1);
+                for (int i = 0; i < n; ++i, ++sc) {
+                    const int pb = sc & 1;
+                    tc_fence_after();
+                    const uint32_t pf_a = smem_u32(&bars->p_full[pb ^ 1]), pf_p = ((sc + 1) >> 1) & 1;
+                    const bool r = mbar_test(pf_a, pf_p);   // step i+1's P^T / dS^T
+                    const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
+                    const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
+                    const uint64_t dsd = ds_mn + ((uint32_t)(pb * DS_BYTES) >> 4);
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < BN / 16; ++kk) {
+                            // queries [16 kk, 16 kk + 16): packed by warpgroup kk / 2 at column 32 (kk / 2) + 8 (kk % 2)
+                            const uint32_t ca = (kk >> 1) * 32 + (kk & 1) * 8;
+                            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                            umma_ts(tmem + DV_COL, a_p + ca, dda + kk * (2048 >> 4), idesc_a, acc);
+                            umma_ts(tmem + DK_COL, a_d + ca, dq + kk * (2048 >> 4), idesc_a, acc);
+                        }
+                        umma_commit(&bars->qa_empty[st_a]);
+#pragma unroll
+                        for (int kk = 0; kk < BM / 16; ++kk)   // keys [16 kk, 16 kk + 16): 16 rows of 128 B
+                            umma_ss(a_p, kt_mn + kk * (2048 >> 4), dsd + kk * (2048 >> 4), idesc_q, kk > 0 ? 1u : 0u);
+                        umma_commit(&bars->dq_full[pb]);
+                        if (i == n - 1) {
+                            umma_commit(&bars->acc_full);
+                            umma_commit(&bars->kv_empty);   // K (dQ^T) and V (dP^T) read
+                        }
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (++st_a == STAGES) st_a = 0;
+                    if (i + 1 < n && !r) mbar_wait_addr(pf_a, pf_p);
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 12) {
+        // ============================================================ P / dS epilogue
+        const int wg = (warp - 4) >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
+        const float ha = 0.5f * a.alpha;
+        int sc = 0, ki = 0;
+        for (;; ++ki) {
+            const int w = ring_take(&bars->ring, ki, lane);
+            if (w < 0) break;
+            const WorkItem it = a.items[w];
+            const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
+            const int k0 = it.tile * BM;
+            const int n = n_qtiles(k0, L, a.K1, a.K2);
+            const int kp = k0 + r;
+            const bool kok = kp < L;
+            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
+            for (int i = 0; i < n; ++i, ++sc) {
+                const int sb = sc & 1;
+                const int qb = (k0 / BN + i) * BN + 32 * wg;   // this warpgroup's 32 queries
+                const int32_t tcur = col_time(cx, qb, lane);
+                const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
+                mbar_wait_sleep(&bars->s_full[sb], (sc >> 1) & 1);
+                __syncwarp();   // tcgen05.ld is .sync.aligned: reconverge after the per-lane wait loop
+                tc_fence_after();
+                float sv[32], dp[32];
+                tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * wg, sv);
+                tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * wg, dp);
+                tmem_ld_wait();
+                float hx[32];
+                k_h(cx, ch, tk, sv, hx);
+                if (ch.flags & FLAG_M) {          // h = 0 and dP = 0 -> P = dS = 0
+                    const uint32_t m = k_vis_bits(cx, kp, kok, qb);
+                    apply_vis(hx, m);
+                    apply_vis(dp, m);
+                }
+                uint32_t p2[16], d2[16];
+                const uint64_t one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {   // fp32 pairs: P = h (1 + t), dS = dP (1 + t)(1 + h (1 - t))
+                    const uint64_t H = f2_pack(hx[2 * c], hx[2 * c + 1]);
+                    const uint64_t T = f2_pack(tanh_approx(hx[2 * c]), tanh_approx(hx[2 * c + 1]));
+                    const uint64_t A1 = fadd2(T, one2);
+                    const float2 pv = f2_unpack(fmul2(H, A1));
+                    p2[c] = pack_bf16(pv.x, pv.y);
+                    const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
+                    const float2 dv = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * c], dp[2 * c + 1]), A1), W));
+                    d2[c] = kok ? pack_bf16(dv.x, dv.y) : 0u;   // keys beyond L must not reach dQ
+                }
+                // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
+                tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);
+                tmem_st16(tmem + lane_base + DP_COL + sb * BN + 32 * wg, d2);
+                // dS^T -> shared memory (B operand of dQ^T, input of the d rab reduction)
+                mbar_wait(&bars->ds_free[sb], ((sc >> 1) - 1) & 1);
+                store_row32_packed(sDS + sb * DS_BYTES, r, 32 * wg, d2);
+                fence_proxy_async_smem();
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+            }
+            mbar_wait_sleep(&bars->acc_full, ki & 1);
+            __syncwarp();
+            tc_fence_after();
+            {   // dV then dK (64 registers at a time under the 512-thread register budget)
+                float acc[64];
+                tmem_ld32(tmem + lane_base + DV_COL + wg * 64, acc);
+                tmem_ld32(tmem + lane_base + DV_COL + wg * 64 + 32, acc + 32);
+                tmem_ld_wait();
+                if (kok) store_out_row64(a.dv, a.ld_grad, o + kp, h * DH + wg * 64, acc, a.gv, a.ld_gate, a.inv_n);
+                tmem_ld32(tmem + lane_base + DK_COL + wg * 64, acc);
+                tmem_ld32(tmem + lane_base + DK_COL + wg * 64 + 32, acc + 32);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->acc_empty);
+                if (kok) store_out_row64(a.dk, a.ld_grad, o + kp, h * DH + wg * 64, acc, a.gk, a.ld_gate, ha * a.inv_n);
+            }
+        }
+    } else if (warp >= 12) {
+        // ============================================================ dQ + d rab
+        const int wq = warp & 3;
+        const int r = wq * 32 + lane;                       // key row of this thread (d rab)
+        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;   // TMEM lanes = dh [32 wq, 32 wq + 32)
+        float* stg = sDQ + wq * (STG_BYTES / 4);
+        const bool rab = a.dpos || a.dts;
+        const float rscale = 0.5f * a.inv_n;                // ds = rscale * ds'
+        float far_acc = 0.f;
+        float dpr[kMaxNearT];
+#pragma unroll
+        for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
+        float* const tsl_l = tsl + wq * 1024 + lane;
+        int sc = 0, ki = 0;
+        for (;; ++ki) {
+            const int w = ring_take(&bars->ring, ki, lane);
+            if (w < 0) break;
+            const WorkItem it = a.items[w];
+            const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
+            const int k0 = it.tile * BM;
+            const int n = n_qtiles(k0, L, a.K1, a.K2);
+            const int kp = k0 + r;
+            const bool kok = kp < L;
+            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
+            for (int i = 0; i < n; ++i, ++sc) {
+                const int sb = sc & 1;
+                const int qb0 = (k0 / BN + i) * BN;
+                mbar_wait_sleep(&bars->dq_full[sb], (sc >> 1) & 1);
+                __syncwarp();
+                tc_fence_after();
+                float v[BN];
+                tmem_ld32(tmem + lane_base + S_COL + sb * BN, v);
+                tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32, v + 32);
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->s_free[sb]);
+                // [64 queries][32 dh] box -> TMA add into the fp32 accumulator (rows past L add zeros)
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < BN; ++q) stg[q * 32 + lane] = v[q];
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_reduce_add_2d(&tmDQ, stg, h * DH + 32 * wq, o + qb0);
+                    bulk_commit();
+                }
+                if (rab) {
+                    mbar_wait(&bars->p_full[sb], (sc >> 1) & 1);   // the P/dS warps' shared stores are visible
+                    const uint8_t* row = sDS + sb * DS_BYTES + r * 128;
+#pragma unroll 1
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const int qb = qb0 + 32 * hf;
+                        const int32_t tcur = col_time(cx, qb, lane);
+                        const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
+                        uint32_t d2[16];
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 u = *reinterpret_cast<const uint4*>(row + (((4 * hf + c) ^ (r & 7)) << 4));
+                            d2[4 * c] = u.x; d2[4 * c + 1] = u.y; d2[4 * c + 2] = u.z; d2[4 * c + 3] = u.w;
+                        }
+                        const float tsum = sum_packed16(d2);   // rows beyond L carry zeros
+                        if (a.dts) {
+                            if (!(ch.flags & FLAG_T2)) {
+                                float so = 0.f;                // columns [n, 32) are in bucket b_other (FLAG_T1)
+                                if ((ch.flags & FLAG_T1) && ch.n < 32) {
+                                    uint32_t m2[16];
+#pragma unroll
+                                    for (int e = 0; e < 16; ++e)
+                                        m2[e] = d2[e] & (2 * e >= ch.n ? 0xFFFFFFFFu : (2 * e + 1 >= ch.n ? 0xFFFF0000u : 0u));
+                                    so = sum_packed16(m2);
+                                    if (kok) tsl_l[ch.b_other * 32] += so;
+                                }
+                                if (kok) tsl_l[ch.b_base * 32] += tsum - so;
+                            } else {                           // next to the diagonal: per-element buckets,
+                                int bk[32];                    // monotone along the row (runs flushed on change)
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) bk[c] = bucket32(__shfl_sync(0xffffffffu, ch.tcol, c) - tk, cx.NB);
+                                if (kok) {
+                                    int cur = bk[0];
+                                    float acc = 0.f;
+#pragma unroll
+                                    for (int c = 0; c < 32; ++c) {
+                                        const float2 u = unpack_bf16x2(d2[c >> 1]);
+                                        if (bk[c] != cur) { tsl_l[cur * 32] += acc; cur = bk[c]; acc = 0.f; }
+                                        acc += (c & 1) ? u.y : u.x;
+                                    }
+                                    tsl_l[cur * 32] += acc;
+                                }
+                            }
+                        }
+                        far_acc += tsum;
+                        // near diagonals: delta = q - k = C + c - lane with C a multiple of 32; a
+                        // skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
+                        if (a.dpos) {
+                            const int C = qb - k0 - 32 * wq;
+                            if (C >= -31 && C <= a.P + 29) {   // warp-uniform
+                                float lo_s = 0.f, hi_s = 0.f;
+#pragma unroll
+                                for (int c = 0; c < 32; ++c) {
+                                    const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (c - lane) & 31));
+                                    const float xv = (c & 1) ? u.y : u.x;
+                                    if (c >= lane) lo_s += xv; else hi_s += xv;
+                                }
+                                const int dlo = C + lane, dhi = C + lane - 32;
+                                const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
+                                const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
+#pragma unroll
+                                for (int t = 0; t < kMaxNearT; ++t) {
+                                    dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
+                                    dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
+                                }
+                                far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->ds_free[sb]);
+            }
+        }
+        if (lane == 0) bulk_wait0();
+        __syncwarp();
+        // ---- CTA-level reduction of the d rab partials, then one global atomic per entry
+        if (rab) {
+            const int et = threadIdx.x - 384;                    // 0..127 among the dQ warps
+            float* redp = sDQ;                                   // [kMaxNearT*32][4 warps] + far[4]
+            named_bar_sync(3, 128);                              // every warp's last TMA add has read its box
+            if (a.dpos) {
+#pragma unroll
+                for (int t = 0; t < kMaxNearT; ++t) redp[(t * 32 + lane) * 4 + wq] = dpr[t];
+            }
+            float f = far_acc;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
+            if (lane == 0) redp[kMaxNearT * 32 * 4 + wq] = f;
+            named_bar_sync(3, 128);
+            if (a.dts) {                       // bucket et >> 2, warp et & 3: 32 lanes, then 4 warps
+                const int b = et >> 2, w4 = et & 3;
+                float sum = 0.f;
+#pragma unroll 8
+                for (int l = 0; l < 32; ++l) sum += tsl[(w4 * 32 + b) * 32 + l];
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                if (w4 == 0 && b < a.NB && sum != 0.f) atomicAdd(a.dts + b, sum * rscale);
+            }
+            if (a.dpos) {
+                for (int e = et; e < a.P - 1; e += 128) {
+                    float sum = 0.f;
+#pragma unroll
+                    for (int w4 = 0; w4 < 4; ++w4) sum += redp[e * 4 + w4];
+                    if (sum != 0.f) atomicAdd(a.dpos + e, sum * rscale);
+                }
+                if (et == 0) {
+                    float sum = 0.f;
+#pragma unroll
+                    for (int w4 = 0; w4 < 4; ++w4) sum += redp[kMaxNearT * 32 * 4 + w4];
+                    if (sum != 0.f) atomicAdd(a.dpos + a.P - 1, sum * rscale);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// dQ = alpha/(2N) * acc (x gate), bf16, into its slice of dH
+__global__ void __launch_bounds__(256) dq_finish_k(int64_t T, int width, const float* __restrict__ acc, int64_t lda,
+                                                   const __nv_bfloat16* __restrict__ gate, int64_t ldg, float scale,
+                                                   __nv_bfloat16* __restrict__ dq, int64_t ldq) {
+    const int nch = width / 8;
+    const int64_t total = T * nch;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / nch;
+        const int c = (int)(i - row * nch) * 8;
+        const float4 a0 = __ldcs(reinterpret_cast<const float4*>(acc + row * lda + c));
+        const float4 a1 = __ldcs(reinterpret_cast<const float4*>(acc + row * lda + c + 4));
+        float v[8] = {a0.x * scale, a0.y * scale, a0.z * scale, a0.w * scale,
+                      a1.x * scale, a1.y * scale, a1.z * scale, a1.w * scale};
+        if (gate) {
+            const uint4 g = __ldg(reinterpret_cast<const uint4*>(gate + row * ldg + c));
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(g2[e]);
+                v[2 * e] *= f.x;
+                v[2 * e + 1] *= f.y;
+            }
+        }
+        *reinterpret_cast<uint4*>(dq + row * ldq + c) =
+            make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+    }
+}
+}  // namespace fb
+
+
 }  // namespace
+
+static bool bwd_split() {   // UH_ATTN_BWD=split selects the two-kernel backward (A/B measurements)
+    static const int v = [] { const char* e = getenv("UH_ATTN_BWD"); return e && !strcmp(e, "split") ? 1 : 0; }();
+    return v != 0;
+}
+
+bool attn_bwd_fused() { return !bwd_split(); }
 
 uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStream_t st, int64_t T) {
     if (aq.dh != DH) return fail(UH_ERR_UNSUPPORTED, "bf16 attention requires head_dim == 128");
-    if (aq.n_items == 0) return UH_OK;
+    if (akv.n_items == 0) return UH_OK;
     const uint64_t width = (uint64_t)aq.H * DH;
+    const int sms = num_sms();
+    if (!bwd_split()) {
+        CUtensorMap q64, dA64, k128, v128, dqm;
+        UH_TRY(make_tmap_bf16(&q64, akv.q, width, T, akv.ld_qkv, 64, fb::BN));
+        UH_TRY(make_tmap_bf16(&dA64, akv.dout, width, T, akv.ld_dout, 64, fb::BN));
+        UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));
+        UH_TRY(make_tmap_bf16(&v128, akv.v, width, T, akv.ld_qkv, 64, 128));
+        UH_TRY(make_tmap_f32(&dqm, akv.dq_acc, width, T, akv.ld_acc, 32, fb::BN));
+        UH_CUDA(cudaMemsetAsync(akv.dq_acc, 0, (size_t)T * akv.ld_acc * sizeof(float), st));
+        UH_CUDA(cudaFuncSetAttribute(fb::attn_bwd_fused_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, fb::SMEM));
+fb::attn_bwd_fused_sm100<<<akv.n_items < sms ? akv.n_items : sms, fb::THREADS, fb::SMEM, st>>>(
+            q64, k128, v128, dA64, dqm, akv);
+        note_launch();
+        UH_CUDA(cudaGetLastError());
+        fb::dq_finish_k<<<4 * sms, 256, 0, st>>>(T, (int)width, akv.dq_acc, akv.ld_acc,
+                                                 (const __nv_bfloat16*)akv.gq, akv.ld_gate, 0.5f * akv.alpha * akv.inv_n,
+                                                 (__nv_bfloat16*)akv.dq, akv.ld_grad);
+        note_launch();
+        UH_CUDA(cudaGetLastError());
+        return UH_OK;
+    }
     CUtensorMap q128, dA128, k64, v64;
     UH_TRY(make_tmap_bf16(&q128, aq.q, width, T, aq.ld_qkv, 64, 128));
     UH_TRY(make_tmap_bf16(&dA128, aq.dout, width, T, aq.ld_dout, 64, 128));
     UH_TRY(make_tmap_bf16(&k64, aq.k, width, T, aq.ld_qkv, 64, 64));
     UH_TRY(make_tmap_bf16(&v64, aq.v, width, T, aq.ld_qkv, 64, 64));
     UH_CUDA(cudaFuncSetAttribute(dq::attn_bwd_dq_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, dq::SMEM));
-    const int sms = num_sms();
     dq::attn_bwd_dq_sm100<<<aq.n_items < sms ? aq.n_items : sms, NUM_THREADS, dq::SMEM, st>>>(q128, k64, v64, dA128, aq);
     note_launch();
     UH_CUDA(cudaGetLastError());

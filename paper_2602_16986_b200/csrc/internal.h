@@ -29,6 +29,9 @@ uh_status cuda_fail(cudaError_t e, const char* where);
 // bf16 2-D tensor map, 128-byte swizzle, box {box_inner, box_outer}
 uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                          uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128);
+// fp32 2-D tensor map, no swizzle (TMA reduce-add targets)
+uh_status make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                        uint32_t box_inner, uint32_t box_outer);
 int num_sms();
 // every kernel launch of the library is counted (bench.py reports gpu_launches from it)
 void note_launch();
