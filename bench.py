@@ -324,24 +324,32 @@ def run_ours(args, rank, world, local_rank):
 
 
 def roofline_bwd(bwd_flop: float, bwd_ms: float, peaks: dict, workload: str):
-    """The dominant step, attention backward (B4: attn_bwd_dq_sm100 + attn_bwd_dkv_sm100 in one
-    uh_attn_bwd call), against the measured bf16 burst peak (timed alone).  achieved =
-    10 d_h H nnz algorithmic FLOPs per launch / the CUDA-event launch time; traffic = DRAM
-    read + write bytes of the two kernels per launch from the committed ncu --set full capture
-    of the same workload (profiles/r01_ncu_attn_cfg3.json)."""
+    """The dominant step, attention backward (B4, one uh_attn_bwd call: the fused key-major
+    kernel attn_bwd_fused_sm100 plus the dQ finish kernel; UH_ATTN_BWD=split selects the
+    two-kernel path) against the measured bf16 burst peak (timed alone).  achieved = 10 d_h H nnz
+    algorithmic FLOPs per launch / the CUDA-event time of the call; traffic = DRAM read + write
+    bytes per launch of the call's kernels from the committed ncu --set full capture of the same
+    workload (profiles/r01_ncu_attn_fused_cfg3.json; split: profiles/r01_ncu_attn_cfg3.json)."""
     achieved = bwd_flop / (bwd_ms / 1e3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_ncu_attn_cfg3.json")
+    split = os.environ.get("UH_ATTN_BWD") == "split"
+    name = "r01_ncu_attn_cfg3.json" if split else "r01_ncu_attn_fused_cfg3.json"
+    prof = os.path.join(ROOT, "profiles", name)
     if workload == "cfg3" and os.path.exists(prof):
         with open(prof) as f:
             pr = json.load(f)
-        traffic = sum(pr[k]["dram_read_bytes"] + pr[k]["dram_write_bytes"] for k in ("dq", "dkv"))
-    return {"kernel": "attention backward (attn_bwd_dq_sm100 + attn_bwd_dkv_sm100, one uh_attn_bwd call)",
+        keys = ("dq", "dkv") if split else ("fused", "dq_finish")
+        traffic = sum(pr[k]["dram_read_bytes"] + pr[k]["dram_write_bytes"] for k in keys)
+    kern = ("attn_bwd_dq_sm100 + attn_bwd_dkv_sm100" if split else
+            "attn_bwd_fused_sm100 + dq_finish_k (+ a cudaMemsetAsync of the fp32 dQ accumulator)")
+    return {"kernel": f"attention backward ({kern}, one uh_attn_bwd call)",
             "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16_tflops"], "peak_source": peaks["source"] + " (burst: timed alone)",
             "algorithmic_flop_per_launch": bwd_flop, "traffic": traffic,
-            "traffic_note": "DRAM bytes per launch (ncu --set full, profiles/r01_ncu_attn_cfg3.json); "
-                            "algorithmic minimum ~1.6e9 (read Q, K, V, dA; write dQ, dK, dV)"}
+            "traffic_note": f"DRAM bytes per launch (ncu --set full, profiles/{name}; the memset's 0.54 GB write is "
+                            "not in it); algorithmic minimum ~1.6e9 (read Q, K, V, dA; write dQ, dK, dV) plus the "
+                            "fp32 dQ accumulator (fused: 0.54 GB zeroed by the memset, read once by the finish "
+                            "kernel; 61% of the dQ reduction sectors miss L2 at cfg3, the bulk of the excess)"}
 
 
 # ----------------------------------------------------------------------------- cfg5: inference
