@@ -1,0 +1,125 @@
+"""Regenerate profiles/r01_summary.md from the committed bench lines, the ncu launch list and
+the ncu --set full summaries (no GPU needed)."""
+import csv
+import json
+import os
+from collections import OrderedDict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles")
+
+# launches per layer step (the launch list also holds the bench's attention-only timing calls)
+PER_STEP = {"ln_fwd_k": 1, "gemm_bf16_sm100<256, 0, 1, 1, 1>": 2, "build_schedule_k": 2, "attn_fwd_sm100": 1,
+            "gated_fwd_k": 1, "gemm_bf16_sm100<256, 0, 1, 0, 1>": 1, "ln_apply_k": 1, "gemm_bf16_sm100<256, 0, 0, 0, 1>": 1,
+            "gated_bwd_k": 1, "gemm_bf16_sm100<256, 1, 1, 2, 2>": 2, "attn_bwd_fused_sm100": 1, "dq_finish_k": 1,
+            "gemm_bf16_sm100<256, 0, 0, 0, 2>": 1, "ln_bwd_k": 1, "colsum_k": 0, "FillFunctor": 0}
+
+LABELS = [
+    ("ln_fwd_k", "F1 LN"),
+    ("gemm_bf16_sm100<256, 0, 1, 1, 1>", "F2 f1+SiLU / B3 remat (+silu')"),
+    ("build_schedule_k", "F0 schedule"),
+    ("attn_fwd_sm100", "F3-F5 attention fwd"),
+    ("gated_fwd_k", "F6 gated norm"),
+    ("gemm_bf16_sm100<256, 0, 1, 0, 1>", "F7 f2 + residual"),
+    ("ln_apply_k", "B3 x^ remat"),
+    ("gemm_bf16_sm100<256, 0, 0, 0, 1>", "B1 dY"),
+    ("gated_bwd_k", "B2 gated-norm bwd"),
+    ("gemm_bf16_sm100<256, 1, 1, 2, 2>", "B1 dW2+db2 / B5 dW1+db1 (split-K, fused column sums)"),
+    ("attn_bwd_fused_sm100", "B4 attention bwd (fused dK, dV, dQ)"),
+    ("dq_finish_k", "B4 dQ finish (fp32 accumulator -> bf16 x silu')"),
+    ("attn_bwd_dq_sm100", "B4 attention bwd dQ (split)"),
+    ("attn_bwd_dkv_sm100", "B4 attention bwd dK,dV (split)"),
+    ("gemm_bf16_sm100<256, 0, 0, 0, 2>", "B5 dx^ (256x256 tiles)"),
+    ("ln_bwd_k", "B6 LN bwd"),
+    ("colsum_k", "B1 db2 / B5 db1"),
+    ("FillFunctor", "(torch fill, bench harness)"),
+]
+
+
+def label(name):
+    for k, v in LABELS:
+        if k in name:
+            return v
+    return "?"
+
+
+def launches():
+    rows = [r for r in csv.reader(open(os.path.join(P, "r01_bench_launches.csv"))) if len(r) > 10]
+    h = rows[0]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    d = OrderedDict()
+    for r in rows[1:]:
+        nm = r[ki].split("(")[0].replace("void ", "").replace("uh::<unnamed>::", "::").replace("uh::", "")
+        full = r[ki]
+        key = nm if "gemm" not in nm else full.split("(")[0].replace("void uh::", "")
+        d.setdefault(key, []).append(float(r[vi].replace(",", "")) / 1e3)
+    return d
+
+
+def main():
+    b = json.load(open(os.path.join(P, "r01_bench.json")))
+    at, rf = b["attn"], b["roofline"]
+    out = ["# Round 1 profile summary (cfg3: 16 x 16384 tokens, 4 x 128 heads, SLA 1024 + 128 global, rab on)", ""]
+    out += ["## Bench line (`python bench.py`, one B200): `r01_bench.json`", ""]
+    out += [f"Layer step {b['ms_per_step']:.2f} ms = {b['value'] / 1e6:.1f} M tokens/s. Attention fwd {at['fwd_ms']:.3f} ms / "
+            f"bwd {at['bwd_ms']:.3f} ms = {at['effective_tflops']:.0f} TFLOP/s effective "
+            f"({100 * at['frac_of_measured_bf16_burst']:.1f}% of the measured bf16 burst). Roofline (attention backward): "
+            f"{rf['achieved']:.0f} / {rf['peak']:.0f} TFLOP/s = {rf['frac']:.3f}; traffic {rf['traffic'] / 1e9:.2f} GB per launch. "
+            f"e2e {b['e2e']['value'] / 1e6:.1f} M tokens/s; clocks {b['clocks']['sm_mhz']} / {b['clocks']['sm_max_mhz']} MHz "
+            f"{b['clocks']['reasons']}; {b['gpu_launches']} kernel launches in the timed region.", ""]
+    for n in (2, 4):
+        f = os.path.join(P, f"r01_bench_{n}gpu.json")
+        if os.path.exists(f):
+            d = json.loads(open(f).read().strip().splitlines()[-1])
+            out.append(f"{n} GPUs (`r01_bench_{n}gpu.json`): {d['value'] / 1e6:.1f} M tokens/s at {d['ms_per_step']:.2f} ms "
+                       f"per step (weak scaling, {100 * d['value'] / (n * b['value']):.0f}% of {n} x one GPU).")
+    for n in (1, 2, 4):
+        f = os.path.join(P, f"r01_bench_cfg4_{n}gpu.json")
+        if os.path.exists(f):
+            d = json.loads(open(f).read().strip().splitlines()[-1])
+            out.append(f"cfg4 (18-layer stack, long-tail lengths) on {n} GPU(s) (`r01_bench_cfg4_{n}gpu.json`): "
+                       f"{d['value'] / 1e6:.2f} M tokens/s at {d['ms_per_step']:.1f} ms per step.")
+    out += ["", "## One layer step, launch by launch (ncu `gpu__time_duration.sum --clock-control none`, cold-cache, "
+            "serialised): `r01_bench_launches.csv`", ""]
+    d = launches()
+
+    def per_step(k):
+        for key, n in PER_STEP.items():
+            if key in k:
+                return n
+        return 0
+    tot = sum(sum(v) / len(v) * per_step(k) for k, v in d.items())
+    out += ["| step | kernel | launches per step | us per launch | us per step | share |", "|---|---|---|---|---|---|"]
+    for k, v in d.items():
+        n = per_step(k)
+        if n == 0:
+            continue
+        per = sum(v) / len(v) * n
+        out.append(f"| {label(k)} | `{k}` | {n} | {sum(v) / len(v):.1f} | {per:.1f} | {100 * per / tot:.1f}% |")
+    out += [f"| | **total** | | | {tot:.0f} | |", ""]
+    fz = json.load(open(os.path.join(P, "r01_ncu_attn_fused_cfg3.json")))
+    out += ["## Attention backward, `ncu --set full` (tools/gpu_prof_fused.sh): `r01_ncu_attn_fused_cfg3.json`", "",
+            "| kernel | duration (us) | tensor pipe active % | issue active % | DRAM read GB | DRAM write GB | L2 hit % | "
+            "dQ reduction sectors missing L2 | regs |", "|---|---|---|---|---|---|---|---|---|"]
+    for k in ("fused", "dq_finish"):
+        x = fz[k]
+        miss = f"{100 * x['l2_red_miss_sectors'] / x['l2_red_sectors']:.0f}%" if x.get("l2_red_sectors") else "-"
+        out.append(f"| `{k}` | {x['duration_ns'] / 1e3:.0f} | {x.get('tensor_pipe_active_pct', 0):.1f} | "
+                   f"{x['issue_active_pct']:.1f} | {x['dram_read_bytes'] / 1e9:.2f} | {x['dram_write_bytes'] / 1e9:.2f} | "
+                   f"{x['l2_hit_pct']:.0f} | {miss} | {x['regs']:.0f} |")
+    out += ["", "Algorithmic DRAM bytes per backward launch: read Q, K, V, dA (1.07 GB), write dK, dV (0.54 GB), and the "
+            "fp32 dQ accumulator (0.54 GB zeroed, 0.54 GB read by the finish kernel, 0.27 GB bf16 dQ written). The fused "
+            "kernel's excess DRAM traffic is the accumulator's lines leaving L2 between the ~10 key tiles that add into "
+            "them (61% of the reduction sectors miss).", ""]
+    sp = json.load(open(os.path.join(P, "r01_ncu_attn_cfg3.json")))
+    out += ["Earlier split path (`r01_ncu_attn_cfg3.json`, UH_ATTN_BWD=split): forward "
+            f"{sp['fwd']['duration_ns'] / 1e3:.0f} us, dQ {sp['dq']['duration_ns'] / 1e3:.0f} us, dK/dV "
+            f"{sp['dkv']['duration_ns'] / 1e3:.0f} us.", "",
+            "## cfg5 inference: `r01_cfg5_inference.md`", "",
+            "## Microbenchmarks (`tools/micro/`, run with `gpurun`): see DESIGN.md §5.9", ""]
+    open(os.path.join(P, "r01_summary.md"), "w").write("\n".join(out))
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main()
