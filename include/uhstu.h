@@ -126,7 +126,10 @@ UH_API int64_t uh_mask_nnz(uh_mask m, int64_t L);
 /* Sum over the batch of uh_mask_nnz (host; reads host_offsets). */
 UH_API int64_t uh_batch_nnz(const uh_jagged* jag, uh_mask m);
 
-/* Workspace bytes for uh_attn_fwd (backward=0) or uh_attn_bwd (backward=1). */
+/* Workspace bytes for uh_attn_fwd (backward=0) or uh_attn_bwd (backward=1).  The bf16
+ * backward's workspace holds the tile schedule and an fp32 [T, H*head_dim] dQ accumulator
+ * (4 bytes per token and dQ column; zeroed inside the call), so it is ~T*H*head_dim*4 bytes;
+ * with UH_ATTN_BWD=split in the environment it holds the two tile schedules only. */
 UH_API uh_status uh_attn_workspace_bytes(const uh_jagged* jag, uh_mask m, const uh_attn_desc* desc,
                                   uh_dtype dtype, int backward, size_t* bytes);
 
@@ -139,6 +142,9 @@ UH_API uh_status uh_attn_fwd(const uh_jagged* jag, uh_mask m, const uh_attn_desc
 
 /* Attention backward (Listing 1 "attention_backward(dattn, q, k, v)").
  * dout: dL/dA, row stride ld_dout.  dq, dk, dv: overwritten, row stride ld_grad.
+ * bf16: one key-major kernel computes dK, dV and the dQ partials (reduced into the
+ * workspace's fp32 accumulator), then a finish kernel writes dq; the call is stream-ordered
+ * and CUDA-graph capturable (a cudaMemsetAsync zeroes the accumulator).
  * dpos_bias / dtime_bias: fp32, ACCUMULATED into (caller zeroes); may be NULL
  * when the matching table is NULL. */
 UH_API uh_status uh_attn_bwd(const uh_jagged* jag, uh_mask m, const uh_attn_desc* desc, uh_dtype dtype,
