@@ -692,6 +692,11 @@ attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
 // L2-resident).  S, P and dP are computed once instead of once per kernel.  The same
 // warpgroup reduces d pos_bias / d time_bias from the dS^T tile in shared memory.
 namespace fb {
+#if UH_TRACE == 3   // per-step timeline of CTA 0 (tools/trace_fused.py)
+#define TRACE_FB(ev, sc) do { if (lane == 0) TRACE((ev) * 1024 + ((sc) & 1023)); } while (0)
+#else
+#define TRACE_FB(ev, sc) do { } while (0)
+#endif
 constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per step
 constexpr int KT = BM * DH * 2;           // K / V tile (32 KB: 2 x 16 KB blocks of [128 rows x 128 B])
 constexpr int QT = BN * DH * 2;           // Q / dA tile (16 KB: 2 x 8 KB blocks of [64 rows x 128 B])
@@ -739,6 +744,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
     float* ts_s = pos_s + kPosTab;
     Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TRACE_SETUP();
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1); mbar_init(&bars->kv_empty, 1);
@@ -780,6 +786,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                     const int s = qc % STAGES;
                     uint8_t* st = sQA + s * 2 * QT;
                     mbar_wait_sleep(&bars->qa_empty[s], ((qc / STAGES) & 1) ^ 1);
+                    TRACE_FB(7, qc);
                     mbar_arrive_expect_tx(&bars->qa_full[s], 2 * QT);
                     tma_load_2d(st, &tmQ, &bars->qa_full[s], h * DH, row);
                     tma_load_2d(st + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
@@ -821,6 +828,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                     const bool r1 = mbar_test(qa_a, nph), r2 = mbar_test(sf_a, sf_p);
                     const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
                     const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
+                    TRACE_FB(0, sc);
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < DH / 16; ++kk) {
@@ -859,6 +867,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                     const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
                     const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
                     const uint64_t dsd = ds_mn + ((uint32_t)(pb * DS_BYTES) >> 4);
+                    TRACE_FB(1, sc);
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < BN / 16; ++kk) {
@@ -910,6 +919,8 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
                 mbar_wait_sleep(&bars->s_full[sb], (sc >> 1) & 1);
                 __syncwarp();   // tcgen05.ld is .sync.aligned: reconverge after the per-lane wait loop
+                if (warp == 4) TRACE_FB(2, sc);
+                if (warp == 8) TRACE_FB(4, sc);
                 tc_fence_after();
                 float sv[32], dp[32];
                 tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * wg, sv);
@@ -946,6 +957,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+                if (warp == 4) TRACE_FB(3, sc);
             }
             mbar_wait_sleep(&bars->acc_full, ki & 1);
             __syncwarp();
@@ -995,6 +1007,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 const int qb0 = (k0 / BN + i) * BN;
                 mbar_wait_sleep(&bars->dq_full[sb], (sc >> 1) & 1);
                 __syncwarp();
+                if (warp == 12) TRACE_FB(5, sc);
                 tc_fence_after();
                 float v[BN];
                 tmem_ld32(tmem + lane_base + S_COL + sb * BN, v);
@@ -1086,6 +1099,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_free[sb]);
+                if (warp == 12) TRACE_FB(6, sc);
             }
         }
         if (lane == 0) bulk_wait0();

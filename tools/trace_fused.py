@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 print("bwd ms (traced)", e0.elapsed_time(e1))
 tr = tb.view(8, 1024).cpu().numpy()
 t0 = tr[tr > 0].min()
-names = ["A_issue", "BC_issue", "E1a_sfull", "E1a_pfull", "E1b_sfull", "E2_dqfull", "E2_dsfree", "E2_end"]
+names = ["A_issue", "BC_issue", "E1a_sfull", "E1a_pfull", "E1b_sfull", "E2_dqfull", "E2_dsfree", "QA_load"]
 first = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 cnt = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 for j in range(first, first + cnt):
