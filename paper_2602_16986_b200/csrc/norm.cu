@@ -8,7 +8,12 @@
 // across a grid-stride loop over rows and reduced once per block.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <initializer_list>
+#include <utility>
+
 #include "internal.h"
+#include "sm100.cuh"
 
 namespace uh {
 namespace {
@@ -323,6 +328,227 @@ __global__ void __launch_bounds__(256) ln_bwd_k(int64_t nrows, int d, const T* _
     flush_param_grads<T, CPL>(d, pw, pb, dw, db, red);
 }
 
+// ------------------------------------------------------------------ pipelined backward rows (bf16)
+// The same arithmetic as gated_bwd_k / ln_bwd_k with the rows' inputs streamed into a per-warp
+// shared-memory ring by cp.async.bulk (one lane issues, DEPTH rows ahead): 16 warps per SM
+// keep DEPTH x NT KB in flight each instead of one row, enough to cover HBM latency.
+constexpr int kPipeWarps = 8;
+
+template <int NT, int DEPTH>
+struct RowRing {
+    uint8_t* buf;   // this warp's [DEPTH][NT][row bytes]
+    uint64_t* bar;  // [DEPTH]
+    int rb;
+    __device__ __forceinline__ const uint8_t* slot(int s, int t) const { return buf + (s * NT + t) * rb; }
+    // lane 0: fill slot s with row `row` of the NT sources
+    __device__ __forceinline__ void issue(int s, const uint8_t* const* src, const int64_t* ld_bytes, int64_t row) {
+        fence_proxy_async_smem();   // the warp's generic reads of this slot (synced) precede the async writes
+        mbar_arrive_expect_tx(&bar[s], (uint32_t)(NT * rb));
+#pragma unroll
+        for (int t = 0; t < NT; ++t) bulk_load_1d(buf + (s * NT + t) * rb, src[t] + row * ld_bytes[t], rb, &bar[s]);
+    }
+};
+
+__device__ __forceinline__ void bf16x8_to_f32(uint4 a, float* v) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { float2 f = __bfloat1622float2(h[i]); v[2 * i] = f.x; v[2 * i + 1] = f.y; }
+}
+
+template <int CPL, int DEPTH>
+__global__ void __launch_bounds__(256) gated_bwd_pipe_k(int64_t nrows, int d, const __nv_bfloat16* __restrict__ dY,
+                                                        int64_t lddy, const __nv_bfloat16* __restrict__ A, int64_t lda,
+                                                        const __nv_bfloat16* __restrict__ U, int64_t ldu,
+                                                        const __nv_bfloat16* __restrict__ GU, int64_t ldg,
+                                                        const float* __restrict__ w, const float* __restrict__ b,
+                                                        const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                        __nv_bfloat16* __restrict__ dA, int64_t ldda,
+                                                        __nv_bfloat16* __restrict__ dHU, int64_t ldh,
+                                                        __nv_bfloat16* __restrict__ Y, int64_t ldy, float* dw, float* db) {
+    using T = __nv_bfloat16;
+    constexpr int V = 8, NT = 4;
+    extern __shared__ __align__(128) uint8_t pipe_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb = d * 2, nch = d / V;
+    float* red = reinterpret_cast<float*>(pipe_smem);                     // [2][d] (flush_param_grads)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(pipe_smem + 2 * d * 4);  // [8 warps][DEPTH]
+    uint8_t* ring0 = pipe_smem + 2 * d * 4 + kPipeWarps * DEPTH * 8;
+    ring0 += (128 - (reinterpret_cast<uintptr_t>(ring0) & 127)) & 127;
+    RowRing<NT, DEPTH> rr{ring0 + (size_t)warp * DEPTH * NT * rb, bars + warp * DEPTH, rb};
+    const uint8_t* src[NT] = {reinterpret_cast<const uint8_t*>(A), reinterpret_cast<const uint8_t*>(U),
+                              reinterpret_cast<const uint8_t*>(dY), reinterpret_cast<const uint8_t*>(GU)};
+    const int64_t ldb[NT] = {lda * 2, ldu * 2, lddy * 2, ldg * 2};
+    const int64_t G = (int64_t)gridDim.x * kPipeWarps;
+    const int64_t r0 = (int64_t)blockIdx.x * kPipeWarps + warp;
+    if (lane == 0) {
+        for (int s = 0; s < DEPTH; ++s) mbar_init(&rr.bar[s], 1);
+        fence_barrier_init();
+        for (int s = 0; s < DEPTH; ++s)
+            if (r0 + s * G < nrows) rr.issue(s, src, ldb, r0 + s * G);
+    }
+    __syncwarp();
+    float wv[CPL][V], bv[CPL][V], pw[CPL][V], pb[CPL][V];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+#pragma unroll
+        for (int e = 0; e < V; ++e) { pw[c][e] = 0.f; pb[c][e] = 0.f; wv[c][e] = 0.f; bv[c][e] = 0.f; }
+        if (ch < nch)
+#pragma unroll
+            for (int e = 0; e < V; e += 4) { load4f(w + ch * V + e, wv[c] + e); load4f(b + ch * V + e, bv[c] + e); }
+    }
+    float mu_n = 0.f, rs_n = 0.f;
+    if (r0 < nrows) { mu_n = mean[r0]; rs_n = rstd[r0]; }
+    int k = 0;
+    for (int64_t row = r0; row < nrows; row += G, ++k) {
+        const int s = k % DEPTH;
+        const float mu = mu_n, rs = rs_n;
+        if (row + G < nrows) { mu_n = mean[row + G]; rs_n = rstd[row + G]; }   // next row's stats in flight
+        mbar_wait(&rr.bar[s], (k / DEPTH) & 1);
+        float xt[CPL][V], g[CPL][V];
+        float sg = 0.f, sgx = 0.f;
+        uint4 yo[CPL], ho[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) {
+                float a[V], u[V], dy[V], gu[V], y[V], dh[V];
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 0) + ch * 16), a);
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 1) + ch * 16), u);
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 2) + ch * 16), dy);
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 3) + ch * 16), gu);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    xt[c][e] = (a[e] - mu) * rs;
+                    const float ah = xt[c][e] * wv[c][e] + bv[c][e];
+                    y[e] = ah * u[e];
+                    const float dah = dy[e] * u[e];
+                    dh[e] = dy[e] * ah * gu[e];
+                    g[c][e] = dah * wv[c][e];
+                    pw[c][e] += dah * xt[c][e];
+                    pb[c][e] += dah;
+                    sg += g[c][e];
+                    sgx += g[c][e] * xt[c][e];
+                }
+                Vec<T>::store(reinterpret_cast<T*>(&yo[c]), y);
+                Vec<T>::store(reinterpret_cast<T*>(&ho[c]), dh);
+            }
+        }
+        __syncwarp();   // every lane has read slot s
+        if (lane == 0 && row + DEPTH * G < nrows) rr.issue(s, src, ldb, row + DEPTH * G);
+        const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) {
+                float o[V];
+#pragma unroll
+                for (int e = 0; e < V; ++e) o[e] = rs * (g[c][e] - mg - xt[c][e] * mgx);
+                Vec<T>::store(dA + row * ldda + ch * V, o);
+                *reinterpret_cast<uint4*>(dHU + row * ldh + ch * V) = ho[c];
+                if (Y) *reinterpret_cast<uint4*>(Y + row * ldy + ch * V) = yo[c];
+            }
+        }
+    }
+    flush_param_grads<T, CPL>(d, pw, pb, dw, db, red);
+}
+
+template <int CPL, int DEPTH, bool RES>
+__global__ void __launch_bounds__(256) ln_bwd_pipe_k(int64_t nrows, int d, const __nv_bfloat16* __restrict__ dxh,
+                                                     int64_t ldg, const __nv_bfloat16* __restrict__ x, int64_t ldx,
+                                                     const float* __restrict__ w, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd,
+                                                     const __nv_bfloat16* __restrict__ dres, int64_t ldr,
+                                                     __nv_bfloat16* __restrict__ dx, int64_t lddx, float* dw, float* db) {
+    using T = __nv_bfloat16;
+    constexpr int V = 8, NT = RES ? 3 : 2;
+    extern __shared__ __align__(128) uint8_t pipe_smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb = d * 2, nch = d / V;
+    float* red = reinterpret_cast<float*>(pipe_smem);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(pipe_smem + 2 * d * 4);
+    uint8_t* ring0 = pipe_smem + 2 * d * 4 + kPipeWarps * DEPTH * 8;
+    ring0 += (128 - (reinterpret_cast<uintptr_t>(ring0) & 127)) & 127;
+    RowRing<NT, DEPTH> rr{ring0 + (size_t)warp * DEPTH * NT * rb, bars + warp * DEPTH, rb};
+    const uint8_t* src[3] = {reinterpret_cast<const uint8_t*>(x), reinterpret_cast<const uint8_t*>(dxh),
+                             reinterpret_cast<const uint8_t*>(dres)};
+    const int64_t ldb[3] = {ldx * 2, ldg * 2, ldr * 2};
+    const int64_t G = (int64_t)gridDim.x * kPipeWarps;
+    const int64_t r0 = (int64_t)blockIdx.x * kPipeWarps + warp;
+    if (lane == 0) {
+        for (int s = 0; s < DEPTH; ++s) mbar_init(&rr.bar[s], 1);
+        fence_barrier_init();
+        for (int s = 0; s < DEPTH; ++s)
+            if (r0 + s * G < nrows) rr.issue(s, src, ldb, r0 + s * G);
+    }
+    __syncwarp();
+    float wv[CPL][V], pw[CPL][V], pb[CPL][V];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+#pragma unroll
+        for (int e = 0; e < V; ++e) { pw[c][e] = 0.f; pb[c][e] = 0.f; wv[c][e] = 0.f; }
+        if (ch < nch)
+#pragma unroll
+            for (int e = 0; e < V; e += 4) load4f(w + ch * V + e, wv[c] + e);
+    }
+    float mu_n = 0.f, rs_n = 0.f;
+    if (r0 < nrows) { mu_n = mean[r0]; rs_n = rstd[r0]; }
+    int k = 0;
+    for (int64_t row = r0; row < nrows; row += G, ++k) {
+        const int s = k % DEPTH;
+        const float mu = mu_n, rs = rs_n;
+        if (row + G < nrows) { mu_n = mean[row + G]; rs_n = rstd[row + G]; }
+        mbar_wait(&rr.bar[s], (k / DEPTH) & 1);
+        float xt[CPL][V], g[CPL][V], rv[CPL][V];
+        float sg = 0.f, sgx = 0.f;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) {
+                float xv[V], gv[V];
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 0) + ch * 16), xv);
+                bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 1) + ch * 16), gv);
+                if (RES) bf16x8_to_f32(*reinterpret_cast<const uint4*>(rr.slot(s, 2) + ch * 16), rv[c]);
+#pragma unroll
+                for (int e = 0; e < V; ++e) {
+                    xt[c][e] = (xv[e] - mu) * rs;
+                    g[c][e] = gv[e] * wv[c][e];
+                    pw[c][e] += gv[e] * xt[c][e];
+                    pb[c][e] += gv[e];
+                    sg += g[c][e];
+                    sgx += g[c][e] * xt[c][e];
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && row + DEPTH * G < nrows) rr.issue(s, src, ldb, row + DEPTH * G);
+        const float mg = warp_sum(sg) / d, mgx = warp_sum(sgx) / d;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            const int ch = lane + 32 * c;
+            if (ch < nch) {
+                float o[V];
+#pragma unroll
+                for (int e = 0; e < V; ++e) o[e] = rs * (g[c][e] - mg - xt[c][e] * mgx) + (RES ? rv[c][e] : 0.f);
+                Vec<T>::store(dx + row * lddx + ch * V, o);
+            }
+        }
+    }
+    flush_param_grads<T, CPL>(d, pw, pb, dw, db, red);
+}
+
+constexpr int kPipeDepth = 4;
+template <int NT>
+size_t pipe_smem_bytes(int d) { return (size_t)2 * d * 4 + kPipeWarps * kPipeDepth * 8 + 128 + (size_t)kPipeWarps * kPipeDepth * NT * d * 2; }
+// bf16 rows that the bulk copies can stream: 16-byte aligned rows and bases, d <= 512
+bool pipe_ok(int d, std::initializer_list<std::pair<const void*, int64_t>> ts) {
+    if (d % 8 || d > 512) return false;
+    for (auto& t : ts)
+        if (t.first && ((reinterpret_cast<uintptr_t>(t.first) & 15) || (t.second % 8))) return false;
+    return true;
+}
+
 // ------------------------------------------------------------------ column sums / scale
 // column sums: a block covers cpb 16-byte column vectors x (256 / cpb) row groups; each thread
 // walks its rows with four independent loads in flight, the row groups meet in shared memory,
@@ -414,6 +640,13 @@ int grid_persistent(int64_t T) {
         else return fail(UH_ERR_UNSUPPORTED, "model dim too large for norm kernels"); \
     } while (0)
 
+// pipelined row kernels: d <= 512 (pipe_ok), one or two 16-byte chunks per lane
+#define UH_PIPE_CPL(d, ...)                                                     \
+    do {                                                                        \
+        if ((d) <= 256) { constexpr int CPL = 1; __VA_ARGS__; }                 \
+        else { constexpr int CPL = 2; __VA_ARGS__; }                            \
+    } while (0)
+
 #define UH_DT_DISPATCH(dt, ...)                                    \
     do {                                                           \
         if ((dt) == UH_BF16) { using T = __nv_bfloat16; __VA_ARGS__; } \
@@ -457,6 +690,20 @@ uh_status gated_norm_bwd(uh_dtype dt, int64_t T_, int d, const void* dY, int64_t
                          const float* mean, const float* rstd, void* dA, int64_t ldda, void* dHU, int64_t ldh,
                          void* Y, int64_t ldy, float* dw, float* db, cudaStream_t st) {
     if (T_ == 0) return UH_OK;
+    if (dt == UH_BF16 && pipe_ok(d, {{dY, lddy}, {A, lda}, {U, ldu}, {GU, ldg}, {dA, ldda}, {dHU, ldh}, {Y, ldy}})) {
+        const size_t sm = pipe_smem_bytes<4>(d);
+        const int blocks = (int)std::min<int64_t>(2LL * num_sms(), (T_ + kPipeWarps - 1) / kPipeWarps);
+        using T = __nv_bfloat16;
+        UH_PIPE_CPL(d, {
+            UH_CUDA(cudaFuncSetAttribute(gated_bwd_pipe_k<CPL, kPipeDepth>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            gated_bwd_pipe_k<CPL, kPipeDepth><<<blocks, 256, sm, st>>>(
+                T_, d, (const T*)dY, lddy, (const T*)A, lda, (const T*)U, ldu, (const T*)GU, ldg, w, b, mean, rstd,
+                (T*)dA, ldda, (T*)dHU, ldh, (T*)Y, ldy, dw, db);
+        });
+        note_launch();
+        UH_CUDA(cudaGetLastError());
+        return UH_OK;
+    }
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         gated_bwd_k<T, CPL><<<grid_persistent(T_), 256, 2 * d * sizeof(float), st>>>(
             T_, d, (const T*)dY, lddy, (const T*)A, lda, (const T*)U, ldu, (const T*)GU, ldg, w, b, mean, rstd,
@@ -470,6 +717,28 @@ uh_status ln_bwd(uh_dtype dt, int64_t T_, int d, const void* dxh, int64_t ldg, c
                  const float* w, const float* mean, const float* rstd, const void* dres, int64_t ldr, void* dx,
                  int64_t lddx, float* dw, float* db, cudaStream_t st) {
     if (T_ == 0) return UH_OK;
+    if (dt == UH_BF16 && pipe_ok(d, {{dxh, ldg}, {x, ldx}, {dres, ldr}, {dx, lddx}})) {
+        const int blocks = (int)std::min<int64_t>(2LL * num_sms(), (T_ + kPipeWarps - 1) / kPipeWarps);
+        using T = __nv_bfloat16;
+        if (dres) {
+            const size_t sm = pipe_smem_bytes<3>(d);
+            UH_PIPE_CPL(d, {
+                UH_CUDA(cudaFuncSetAttribute(ln_bwd_pipe_k<CPL, kPipeDepth, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                ln_bwd_pipe_k<CPL, kPipeDepth, true><<<blocks, 256, sm, st>>>(
+                    T_, d, (const T*)dxh, ldg, (const T*)x, ldx, w, mean, rstd, (const T*)dres, ldr, (T*)dx, lddx, dw, db);
+            });
+        } else {
+            const size_t sm = pipe_smem_bytes<2>(d);
+            UH_PIPE_CPL(d, {
+                UH_CUDA(cudaFuncSetAttribute(ln_bwd_pipe_k<CPL, kPipeDepth, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                ln_bwd_pipe_k<CPL, kPipeDepth, false><<<blocks, 256, sm, st>>>(
+                    T_, d, (const T*)dxh, ldg, (const T*)x, ldx, w, mean, rstd, (const T*)dres, ldr, (T*)dx, lddx, dw, db);
+            });
+        }
+        note_launch();
+        UH_CUDA(cudaGetLastError());
+        return UH_OK;
+    }
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         ln_bwd_k<T, CPL><<<grid_persistent(T_), 256, 2 * d * sizeof(float), st>>>(
             T_, d, (const T*)dxh, ldg, (const T*)x, ldx, w, mean, rstd, (const T*)dres, ldr, (T*)dx, lddx, dw, db)));

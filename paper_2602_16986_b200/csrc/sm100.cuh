@@ -102,6 +102,12 @@ UH_DEV void tma_store_2d(const CUtensorMap* map, const void* smem_src, int x, in
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
                  ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(x), "r"(y) : "memory");
 }
+// contiguous global -> shared bulk copy (TMA bulk path), completion counted on an mbarrier;
+// addresses 16-byte aligned, bytes a multiple of 16
+UH_DEV void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 // element-wise add of a shared-memory box into global memory (fp32 tensor map, no swizzle);
 // the reduction happens in L2
 UH_DEV void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int x, int y) {
