@@ -75,8 +75,6 @@ uh_status ln_bwd(uh_dtype dt, int64_t T, int d, const void* dxh, int64_t ldg, co
 // out[c] (+)= sum_rows M[r, c]
 uh_status colsum(uh_dtype dt, int64_t T, int n, const void* M, int64_t ldm, float* out, cudaStream_t st);
 // dst = bf16/f32(acc * G) elementwise over [T, n]
-uh_status scale_store(uh_dtype dt, int64_t T, int n, const float* acc, int64_t lda, const void* G, int64_t ldg,
-                      void* dst, int64_t ldd, cudaStream_t st);
 
 // ------------------------------------------------------------------ attention
 struct AttnCall {

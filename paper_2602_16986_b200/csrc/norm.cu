@@ -1,7 +1,7 @@
 // norm.cu — HBM-bound row kernels of the layer: input LayerNorm (Eq. 1),
 // gated norm Y = Norm(A) (.) U (Eq. 4; "fused gated normalization kernel"
 // P:187) and their backward passes, the x^ rematerialisation from saved statistics
-// ("reusing saved layer-norm statistics"), column sums and the dQ finalise.
+// ("reusing saved layer-norm statistics") and column sums.
 //
 // One warp per row, 16-byte vector accesses (8 bf16 or 4 fp32 per access),
 // coalesced along the row; parameter-gradient partial sums are held in registers
@@ -598,26 +598,6 @@ __global__ void __launch_bounds__(256) colsum_k(int64_t nrows, int n, const T* _
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) scale_store_k(int64_t nrows, int n, const float* __restrict__ acc, int64_t lda,
-                                                     const T* __restrict__ G, int64_t ldg, T* __restrict__ dst,
-                                                     int64_t ldd) {
-    constexpr int V = Vec<T>::N;
-    const int nch = n / V;
-    const int64_t total = nrows * nch;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / nch;
-        const int ch = (int)(i - r * nch);
-        float a[V], gv[V];
-#pragma unroll
-        for (int e = 0; e < V; e += 4) load4f(acc + r * lda + ch * V + e, a + e);
-        Vec<T>::load(G + r * ldg + ch * V, gv);
-#pragma unroll
-        for (int e = 0; e < V; ++e) a[e] *= gv[e];
-        Vec<T>::store(dst + r * ldd + ch * V, a);
-    }
-}
-
-template <typename T>
 int cpl_for(int d) { return (d / Vec<T>::N + 31) / 32; }
 
 int grid_rows(int64_t T) { return (int)((T + kRowsPerBlock - 1) / kRowsPerBlock); }
@@ -765,13 +745,5 @@ uh_status colsum(uh_dtype dt, int64_t T_, int n, const void* M, int64_t ldm, flo
     return UH_OK;
 }
 
-uh_status scale_store(uh_dtype dt, int64_t T_, int n, const float* acc, int64_t lda, const void* G, int64_t ldg,
-                      void* dst, int64_t ldd, cudaStream_t st) {
-    if (T_ == 0 || n == 0) return UH_OK;
-    UH_DT_DISPATCH(dt, scale_store_k<T><<<4 * num_sms(), 256, 0, st>>>(T_, n, acc, lda, (const T*)G, ldg, (T*)dst, ldd));
-    note_launch();
-    UH_CUDA(cudaGetLastError());
-    return UH_OK;
-}
 
 }  // namespace uh
