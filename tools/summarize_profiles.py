@@ -11,8 +11,8 @@ P = os.path.join(ROOT, "profiles")
 # launches per layer step (the launch list also holds the bench's attention-only timing calls)
 PER_STEP = {"ln_fwd_k": 1, "gemm_bf16_sm100<256, 0, 1, 1, 1>": 2, "build_schedule_k": 2, "attn_fwd_sm100": 1,
             "gated_fwd_k": 1, "gemm_bf16_sm100<256, 0, 1, 0, 1>": 1, "ln_apply_k": 1, "gemm_bf16_sm100<256, 0, 0, 0, 1>": 1,
-            "gated_bwd_k": 1, "gemm_bf16_sm100<256, 1, 1, 2, 2>": 2, "attn_bwd_fused_sm100": 1, "dq_finish_k": 1,
-            "gemm_bf16_sm100<256, 0, 0, 0, 2>": 1, "ln_bwd_k": 1, "colsum_k": 0, "FillFunctor": 0}
+            "gated_bwd_k": 1, "gated_bwd_pipe_k": 1, "gemm_bf16_sm100<256, 1, 1, 2, 2>": 2, "attn_bwd_fused_sm100": 1, "dq_finish_k": 1,
+            "gemm_bf16_sm100<256, 0, 0, 0, 2>": 1, "ln_bwd_k": 1, "ln_bwd_pipe_k": 1, "colsum_k": 0, "FillFunctor": 0}
 
 LABELS = [
     ("ln_fwd_k", "F1 LN"),
@@ -23,6 +23,7 @@ LABELS = [
     ("gemm_bf16_sm100<256, 0, 1, 0, 1>", "F7 f2 + residual"),
     ("ln_apply_k", "B3 x^ remat"),
     ("gemm_bf16_sm100<256, 0, 0, 0, 1>", "B1 dY"),
+    ("gated_bwd_pipe_k", "B2 gated-norm bwd (bulk-copy row ring)"),
     ("gated_bwd_k", "B2 gated-norm bwd"),
     ("gemm_bf16_sm100<256, 1, 1, 2, 2>", "B1 dW2+db2 / B5 dW1+db1 (split-K, fused column sums)"),
     ("attn_bwd_fused_sm100", "B4 attention bwd (fused dK, dV, dQ)"),
@@ -30,6 +31,7 @@ LABELS = [
     ("attn_bwd_dq_sm100", "B4 attention bwd dQ (split)"),
     ("attn_bwd_dkv_sm100", "B4 attention bwd dK,dV (split)"),
     ("gemm_bf16_sm100<256, 0, 0, 0, 2>", "B5 dx^ (256x256 tiles)"),
+    ("ln_bwd_pipe_k", "B6 LN bwd (bulk-copy row ring)"),
     ("ln_bwd_k", "B6 LN bwd"),
     ("colsum_k", "B1 db2 / B5 db1"),
     ("FillFunctor", "(torch fill, bench harness)"),
