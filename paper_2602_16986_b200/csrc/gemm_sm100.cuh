@@ -244,9 +244,17 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll 1
             for (int c0 = wg * (BN / 2); c0 < (wg + 1) * (BN / 2); c0 += 32) {
                 float v[32];
+                const int col = nt * BN + c0;
+                // residual row segment (64 B) requested before the accumulator load: the two latencies overlap
+                uint4 rv4[4];
+                const bool use_res = EPI == EPI_BF16 && g.resid && row_ok && col < g.N;
+                if (use_res) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(g.resid + (int64_t)row * g.ldr + col);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) rv4[j] = __ldg(rp + j);
+                }
                 tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + (acc * MSUB + ms) * BN + c0, v);
                 tmem_ld_wait();
-                const int col = nt * BN + c0;
                 if (col >= g.N) continue;   // warp-uniform
                 if (EPI == EPI_F32) {
                     if (!row_ok) continue;
@@ -269,12 +277,10 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (EPI == EPI_BF16) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j) v[j] += hb[j];
-                        if (g.resid && row_ok) {
-                            const uint4* rp = reinterpret_cast<const uint4*>(g.resid + (int64_t)row * g.ldr + col);
+                        if (use_res) {
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                uint4 rv = __ldg(rp + j);
-                                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+                                const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv4[j]);
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
                                     float2 f = __bfloat1622float2(r2[e]);
