@@ -3,6 +3,8 @@
 #include <algorithm>
 
 #include "gemm_sm100.cuh"
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace uh {
@@ -102,9 +104,9 @@ static uh_status gemm_f32(const GemmDesc& g, cudaStream_t st) {
 }
 
 // ============================================================== bf16 tcgen05
-template <int BN, bool AMN, bool BMN, int EPI, int MSUB = 1>
+template <int BN, bool AMN, bool BMN, int EPI, int MSUB = 1, int CG = 1>
 static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
-    using C = GemmCfg<BN, MSUB, EPI>;
+    using C = GemmCfg<BN, MSUB, EPI, CG>;
     CUtensorMap ta, tb;
     if (!AMN) UH_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, C::BM));
     else      UH_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
@@ -118,7 +120,7 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     }
     GemmArgs a;
     a.M = g.M; a.N = g.N; a.K = g.K;
-    a.m_tiles = (g.M + C::BM - 1) / C::BM;
+    a.m_tiles = (g.M + C::BM * CG - 1) / (C::BM * CG);
     a.n_tiles = (g.N + BN - 1) / BN;
     const int nkb = (g.K + C::BK - 1) / C::BK;
     const int sms = num_sms();
@@ -133,9 +135,23 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     a.bias = g.bias; a.resid = (const __nv_bfloat16*)g.resid; a.ldr = g.ldr;
     a.colsum = (EPI == EPI_F32 && BMN && BN == 256) ? g.colsum : nullptr;
     const int total = a.m_tiles * a.n_tiles * a.k_splits;
-    auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI, MSUB>;
+    auto kern = gemm_bf16_sm100<BN, AMN, BMN, EPI, MSUB, CG>;
     UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    kern<<<std::min(total, sms), 384, C::SMEM, st>>>(ta, tb, to0, to1, a);
+    if (CG == 2) {   // CTA pairs: a cluster of two per pair tile
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * std::min(total, sms / 2)));
+        cfg.blockDim = dim3(384);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        UH_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, to0, to1, a));
+    } else {
+        kern<<<std::min(total, sms), 384, C::SMEM, st>>>(ta, tb, to0, to1, a);
+    }
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
@@ -157,7 +173,11 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         return fail(UH_ERR_UNSUPPORTED, "gemm EPI_F32 with mixed majors");
     }
     if (g.a_mn) return fail(UH_ERR_UNSUPPORTED, "gemm bf16-out with MN-major A");
+    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A / MN-major-B projections
+    static const bool pair_ok = [] { const char* e = getenv("UH_GEMM_PAIR"); return !(e && e[0] == '0'); }();
+    const bool pair = pair_ok && wide && g.b_mn;
     if (g.epi == EPI_SILU) {
+        if (pair) return launch_sm100<256, false, true, EPI_SILU, 1, 2>(g, st);
         if (wide) { if (g.b_mn) UH_G(256, false, true, EPI_SILU); UH_G(256, false, false, EPI_SILU); }
         if (g.b_mn) UH_G(128, false, true, EPI_SILU);
         UH_G(128, false, false, EPI_SILU);
@@ -168,6 +188,7 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         if (g.b_mn) return launch_sm100<256, false, true, EPI_BF16, 2>(g, st);
         return launch_sm100<256, false, false, EPI_BF16, 2>(g, st);
     }
+    if (pair && g.K < 1024) return launch_sm100<256, false, true, EPI_BF16, 1, 2>(g, st);
     if (wide) { if (g.b_mn) UH_G(256, false, true, EPI_BF16); UH_G(256, false, false, EPI_BF16); }
     if (g.b_mn) UH_G(128, false, true, EPI_BF16);
     UH_G(128, false, false, EPI_BF16);

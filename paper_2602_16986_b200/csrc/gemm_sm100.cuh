@@ -38,12 +38,15 @@ struct GemmArgs {
 // weight gradients, a 256 x 256 tile streams 64 KB per 1024 MMA cycles instead of 128 x 128's
 // 32 KB per 256 (L2->SM ingress is the limit there).  NACC TMEM accumulators (2 when they fit:
 // the epilogue of tile i overlaps tile i+1's main loop).
-template <int BN, int MSUB = 1, int EPI = 0>
+// CG = 2: a CTA pair computes a 256 x BN tile with cta_group::2 MMAs (M = 256); each CTA holds
+// its 128 A rows and BN/2 B columns per stage, so the per-SM operand traffic through shared
+// memory is that of a 128 x BN/2 tile (the f1 GEMM's 128 x 256 tile is shared-memory bound).
+template <int BN, int MSUB = 1, int EPI = 0, int CG = 1>
 struct GemmCfg {
     static constexpr int BM = 128 * MSUB, BK = 64;
-    static constexpr int STAGES = MSUB == 2 ? 3 : (BN == 256 ? 4 : 6);
+    static constexpr int STAGES = MSUB == 2 ? 3 : (BN / CG == 256 ? 4 : 6);
     static constexpr int A_BYTES = BM * BK * 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int B_BYTES = BN / CG * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     // per epilogue warp a 32x32 bf16 box per output (TMA stores); EPI_F32: [8 row groups][BN] column-sum partials
     static constexpr int STAGING = EPI == 2 ? 8 * BN * 4 : 8 * 2 * 2048;
@@ -52,11 +55,12 @@ struct GemmCfg {
     static constexpr int TMEM_COLS = NACC * MSUB * BN <= 256 ? 256 : 512;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int MSUB = 1>
+template <int BN, bool A_MN, bool B_MN, int EPI, int MSUB = 1, int CG = 1>
 __global__ void __launch_bounds__(384, 1)
 gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1, GemmArgs g) {
-    using C = GemmCfg<BN, MSUB, EPI>;
+    using C = GemmCfg<BN, MSUB, EPI, CG>;
+    static_assert(CG == 1 || (MSUB == 1 && !A_MN && B_MN && BN == 256 && EPI != EPI_F32), "CTA-pair GEMM shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -70,18 +74,25 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     const int warp = threadIdx.x >> 5;
     const int total = g.m_tiles * g.n_tiles * g.k_splits;
+    // CTA pairs: both CTAs walk the same tile sequence; rank 0 (leader) issues the MMAs
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+    const int t_first = (int)blockIdx.x / CG, t_step = (int)gridDim.x / CG;
 
     if (threadIdx.x == 0) {
         // with fused column sums the 8 epilogue warps also read every B stage before it is released
         const int cs_arrivals = (EPI == EPI_F32 && g.colsum) ? 8 : 0;
         for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1 + cs_arrivals); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8 * CG); }
         fence_barrier_init();
     }
     if (warp == 0 && lane_id() == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
-    if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+        else tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync_all();   // the peer's barriers are initialised before any remote use
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -101,10 +112,33 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         // ------------------------------------------------ TMA producer
         if (lane_id() == 0) {
             int stage = 0; uint32_t phase = 0;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int t = t_first; t < total; t += t_step) {
                 int mt, nt, ks, kb0, kb1;
                 decode(t, mt, nt, ks);
                 kb_range(ks, kb0, kb1);
+                if (CG == 2) {   // this CTA's A rows and B columns; the follower counts on the leader's barrier
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* a = sA + stage * C::A_BYTES;
+                        uint8_t* b = sB + stage * C::B_BYTES;
+                        const int arow = mt * 256 + (int)rank * 128, bcol = nt * BN + (int)rank * (BN / 2);
+                        if (rank == 0) {
+                            mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+                            tma_load_2d(a, &tmA, &full[stage], kb * C::BK, arow);
+#pragma unroll
+                            for (int j = 0; j < BN / 128; ++j)
+                                tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], bcol + j * 64, kb * C::BK);
+                        } else {
+                            const uint32_t lb = mapa_shared(smem_u32(&full[stage]), 0);
+                            tma_load_2d_pair(a, &tmA, lb, kb * C::BK, arow);
+#pragma unroll
+                            for (int j = 0; j < BN / 128; ++j)
+                                tma_load_2d_pair(b + j * 64 * C::BK * 2, &tmB, lb, bcol + j * 64, kb * C::BK);
+                        }
+                        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    continue;
+                }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -128,12 +162,12 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 }
             }
         }
-    } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = make_idesc_bf16(128, BN, A_MN, B_MN);
+    } else if (warp == 1 && rank == 0) {
+        // ------------------------------------------------ MMA issuer (CTA pairs: the leader, M = 256)
+        constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
         int stage = 0; uint32_t phase = 0;
         int it = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        for (int t = t_first; t < total; t += t_step, ++it) {
             int mt, nt, ks, kb0, kb1;
             decode(t, mt, nt, ks);
             kb_range(ks, kb0, kb1);
@@ -160,16 +194,21 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         for (int ms = 0; ms < MSUB; ++ms) {   // rows [128 ms, 128 ms + 128) start 16 KB apart (both majors)
                             uint64_t ad = A_MN ? make_sw128_desc(a0 + ms * 16384 + k * 2048, 64 * C::BK * 2, 1024)
                                                : make_sw128_desc(a0 + ms * 16384 + k * 32, 16, 1024);
-                            umma_ss(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                            if (CG == 2) umma_ss_pair(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                            else umma_ss(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                         }
                     }
-                    umma_commit(&empty[stage]);
+                    if (CG == 2) umma_commit_pair(&empty[stage]);
+                    else umma_commit(&empty[stage]);
                 }
                 __syncwarp();
                 stage = nst; phase = nph;
                 if (kb + 1 < kb1 && !rdy) mbar_wait(&full[stage], phase);
             }
-            if (elect_one()) umma_commit(&tfull[acc]);
+            if (elect_one()) {
+                if (CG == 2) umma_commit_pair(&tfull[acc]);
+                else umma_commit(&tfull[acc]);
+            }
             __syncwarp();
         }
     } else if (warp >= 4) {
@@ -179,7 +218,8 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int row_in_tile = wq * 32 + (int)lane_id();
         int it = 0;
         int cs_stage = 0; uint32_t cs_phase = 0;   // B-stage sequence (mirrors the MMA issuer's)
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        const int row_base = CG == 2 ? (int)rank * 128 : 0;   // this CTA's half of a pair tile
+        for (int t = t_first; t < total; t += t_step, ++it) {
             int mt, nt, ks;
             decode(t, mt, nt, ks);
             if (EPI == EPI_F32 && B_MN && BN == 256 && g.colsum) {
@@ -239,7 +279,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             tc_fence_after();
 #pragma unroll 1
             for (int ms = 0; ms < MSUB; ++ms) {
-            const int row = mt * C::BM + ms * 128 + row_in_tile;
+            const int row = mt * C::BM * CG + row_base + ms * 128 + row_in_tile;
             const bool row_ok = row < g.M;
 #pragma unroll 1
             for (int c0 = wg * (BN / 2); c0 < (wg + 1) * (BN / 2); c0 += 32) {
@@ -323,7 +363,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane_id() == 0) {
-                        const int row0 = mt * C::BM + ms * 128 + wq * 32;
+                        const int row0 = mt * C::BM * CG + row_base + ms * 128 + wq * 32;
                         tma_store_2d(&tmO0, box0, col, row0);
                         if (EPI == EPI_SILU && g.out1) tma_store_2d(&tmO1, box1, col, row0);
                         bulk_commit();
@@ -333,12 +373,20 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }   // ms
             tc_fence_before();
             __syncwarp();
-            if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+            if (lane_id() == 0) {
+                if (CG == 2 && rank != 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+                else mbar_arrive(&tempty[acc]);
+            }
         }
     }
     if (warp >= 4 && lane_id() == 0) bulk_wait0();   // TMA stores complete before the CTA retires
     __syncthreads();
-    if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if (CG == 2) {
+        cluster_sync_all();   // both CTAs done with the pair's TMEM
+        if (warp == 2) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+    } else if (warp == 2) {
+        tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    }
 }
 
 }  // namespace uh
