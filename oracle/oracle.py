@@ -19,6 +19,8 @@ silent or garbled).
   d_gated_norm_w, d_linear_w_2) and ``dx += dout``.
 * attention_forward / attention_backward — the C pair loops in attn_oracle.c
   (Eq. 3; SLA mask P:140-146).
+* layer_forward_fp8 / quant_rows_e4m3 / gemm_fp8 — NEXT-2, both projections in
+  row-wise scaled E4M3 (readings R17-R20).
 * partition_lpt — the token-balanced partitioner: LPT on the cost model of
   DESIGN.md §6; the load notion follows LBSL's
   "load of a rank ... sum n_u^gamma" (P:112).
@@ -297,3 +299,84 @@ def partition_lpt(lengths, world: int, d: int, H: int, K1: int, K2: int):
         owner[i] = best
         load[best] += costs[i]
     return owner, load
+
+
+# ----------------------------------------------------------------------------
+# NEXT-2: FP8 projections (§4.2.2 "Mixed-Precision Training and
+# Inference", App. E.1).  "We execute both GEMMs in FP8, while
+# preserving all remaining operations in BF16"; the row-wise scale and
+# quantisation are computed with the preceding layer norms (Fig. fp8).
+# Readings R17-R20: E4M3FN codes, round-to-nearest-even with
+# saturation at 448; activation scale per row s_r = amax_r / 448 (1 for an
+# all-zero row), weight scale per output column; the code is taken in fp32
+# (the kernel's precision: t = fp32(fp32(v) * fp32(448 / amax)), R19).
+# ----------------------------------------------------------------------------
+E4M3_MAX = 448.0
+
+
+def e4m3_round(v):
+    """Nearest E4M3FN value (1 sign, 4 exponent bits with bias 7, 3 mantissa bits;
+    normals 2^-6 .. 448, subnormals k 2^-9), ties to even, |result| <= 448 (R17)."""
+    v = np.asarray(v, np.float64)
+    a = np.abs(v)
+    e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    e = np.maximum(e, -6.0)                 # below 2^-6 the spacing stays 2^-9 (subnormals)
+    ulp = np.exp2(e - 3.0)                  # 3 mantissa bits
+    r = np.round(a / ulp) * ulp             # np.round: half to even; a / ulp is exact
+    r = np.minimum(r, E4M3_MAX)             # satfinite
+    return np.where(a > 0, np.copysign(r, v), 0.0)
+
+
+def quant_rows_e4m3(x):
+    """Row-wise FP8 quantisation (R18, R19).  x [R, C] -> (q [R, C] float64
+    holding E4M3 values, s [R] float64 holding the fp32 scale), x ~= q * s[:, None]."""
+    x32 = np.asarray(x, np.float64).astype(np.float32)
+    amax = np.abs(x32).max(axis=1) if x32.shape[1] else np.zeros(x32.shape[0], np.float32)
+    pos = amax > 0
+    one = np.float32(1.0)
+    safe = np.where(pos, amax, one).astype(np.float32)
+    inv = np.where(pos, np.float32(E4M3_MAX) / safe, one).astype(np.float32)     # fp32 division
+    s = np.where(pos, safe / np.float32(E4M3_MAX), one).astype(np.float32)
+    t = (x32 * inv[:, None]).astype(np.float32)                                   # fp32 product
+    return e4m3_round(t.astype(np.float64)), s.astype(np.float64)
+
+
+def quant_weight_e4m3(w):
+    """Per-output-column quantisation of a weight W [K, N] (R18): returns (qT [N, K]
+    E4M3 values, s [N]) with W[:, n] ~= qT[n, :] * s[n]."""
+    return quant_rows_e4m3(np.asarray(w, np.float64).T)
+
+
+def gemm_fp8(qa, sa, qbT, sb):
+    """Row-wise scaled FP8 GEMM: D = diag(sa) (qa qbT^T) diag(sb), fp64
+    accumulation of the exact code products."""
+    return (np.asarray(qa, np.float64) @ np.asarray(qbT, np.float64).T) * np.asarray(sa)[:, None] \
+        * np.asarray(sb)[None, :]
+
+
+def layer_forward_fp8(x, offsets, prm: LayerParams, H: int, spec: AttnSpec):
+    """Eqs. 1-5 with both projections in FP8: x^ = Norm(x) quantised per row
+    (P:164); h = FP8GEMM(x^, W1) + b1; attention and the gated norm as in
+    layer_forward; Y quantised per row; out = FP8GEMM(Y, W2) + b2 + x (the 2-D bias
+    fused into the GEMM).  Returns (out, cache)."""
+    x = _f64(x)
+    d = x.shape[1]
+    xh, mu1, rs1 = layer_norm(x, _f64(prm.ln1_w), _f64(prm.ln1_b), prm.eps)      # Eq. 1
+    qx, sx = quant_rows_e4m3(xh)                                                  # fused quant (P:164)
+    qw1, sw1 = quant_weight_e4m3(prm.w1)
+    h = gemm_fp8(qx, sx, qw1, sw1)                                                # f1 in FP8 (Eq. 2)
+    if prm.b1 is not None:
+        h = h + _f64(prm.b1)[None, :]
+    s = silu(h)
+    U, V, Q, K = s[:, :d], s[:, d:2 * d], s[:, 2 * d:3 * d], s[:, 3 * d:]
+    A = attention_forward(offsets, H, d // H, Q, K, V, spec)                      # Eq. 3
+    Ah, mu2, rs2 = layer_norm(A, _f64(prm.ln2_w), _f64(prm.ln2_b), prm.eps)
+    Y = Ah * U                                                                    # Eq. 4 inner
+    qy, sy = quant_rows_e4m3(Y)                                                   # fused quant (P:164)
+    qw2, sw2 = quant_weight_e4m3(prm.w2)
+    out = gemm_fp8(qy, sy, qw2, sw2) + x                                          # f2 + 2-D bias (P:165)
+    if prm.b2 is not None:
+        out = out + _f64(prm.b2)[None, :]
+    cache = dict(xh=xh, qx=qx, sx=sx, h=h, U=U, V=V, Q=Q, K=K, A=A, Y=Y, qy=qy, sy=sy,
+                 mu1=mu1, rs1=rs1, mu2=mu2, rs2=rs2)
+    return out, cache

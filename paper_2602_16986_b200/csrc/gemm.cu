@@ -110,7 +110,7 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     CUtensorMap ta, tb;
     if (!AMN) UH_TRY(make_tmap_bf16(&ta, g.A, g.K, g.M, g.lda, 64, C::BM));
     else      UH_TRY(make_tmap_bf16(&ta, g.A, g.M, g.K, g.lda, 64, 64));
-    if (!BMN) UH_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, BN));
+    if (!BMN) UH_TRY(make_tmap_bf16(&tb, g.B, g.K, g.N, g.ldb, 64, BN / CG));   // CTA pairs: each CTA its BN/2 rows
     else      UH_TRY(make_tmap_bf16(&tb, g.B, g.N, g.K, g.ldb, 64, 64));
     // outputs leave through TMA stores of 32x32 boxes (64B swizzle, matching the staging layout)
     CUtensorMap to0 = ta, to1 = ta;
@@ -173,11 +173,15 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         return fail(UH_ERR_UNSUPPORTED, "gemm EPI_F32 with mixed majors");
     }
     if (g.a_mn) return fail(UH_ERR_UNSUPPORTED, "gemm bf16-out with MN-major A");
-    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A / MN-major-B projections
-    static const bool pair_ok = [] { const char* e = getenv("UH_GEMM_PAIR"); return !(e && e[0] == '0'); }();
-    const bool pair = pair_ok && wide && g.b_mn;
+    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A projections; UH_GEMM_PAIR=0
+    // disables them, =1 keeps them to MN-major B (f1, f2), otherwise both B majors (also dY)
+    static const int pair_mode = [] { const char* e = getenv("UH_GEMM_PAIR"); return e ? atoi(e) : 2; }();
+    const bool pair = wide && (pair_mode >= 2 || (pair_mode == 1 && g.b_mn));
     if (g.epi == EPI_SILU) {
-        if (pair) return launch_sm100<256, false, true, EPI_SILU, 1, 2>(g, st);
+        if (pair) {
+            if (g.b_mn) return launch_sm100<256, false, true, EPI_SILU, 1, 2>(g, st);
+            return launch_sm100<256, false, false, EPI_SILU, 1, 2>(g, st);
+        }
         if (wide) { if (g.b_mn) UH_G(256, false, true, EPI_SILU); UH_G(256, false, false, EPI_SILU); }
         if (g.b_mn) UH_G(128, false, true, EPI_SILU);
         UH_G(128, false, false, EPI_SILU);
@@ -188,7 +192,10 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         if (g.b_mn) return launch_sm100<256, false, true, EPI_BF16, 2>(g, st);
         return launch_sm100<256, false, false, EPI_BF16, 2>(g, st);
     }
-    if (pair && g.K < 1024) return launch_sm100<256, false, true, EPI_BF16, 1, 2>(g, st);
+    if (pair && g.K < 1024) {
+        if (g.b_mn) return launch_sm100<256, false, true, EPI_BF16, 1, 2>(g, st);
+        return launch_sm100<256, false, false, EPI_BF16, 1, 2>(g, st);
+    }
     if (wide) { if (g.b_mn) UH_G(256, false, true, EPI_BF16); UH_G(256, false, false, EPI_BF16); }
     if (g.b_mn) UH_G(128, false, true, EPI_BF16);
     UH_G(128, false, false, EPI_BF16);

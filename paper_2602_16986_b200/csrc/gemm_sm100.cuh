@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(384, 1)
 gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1, GemmArgs g) {
     using C = GemmCfg<BN, MSUB, EPI, CG>;
-    static_assert(CG == 1 || (MSUB == 1 && !A_MN && B_MN && BN == 256 && EPI != EPI_F32), "CTA-pair GEMM shape");
+    static_assert(CG == 1 || (MSUB == 1 && !A_MN && BN == 256 && EPI != EPI_F32), "CTA-pair GEMM shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -125,15 +125,23 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         if (rank == 0) {
                             mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
                             tma_load_2d(a, &tmA, &full[stage], kb * C::BK, arow);
+                            if (!B_MN) {
+                                tma_load_2d(b, &tmB, &full[stage], kb * C::BK, bcol);
+                            } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 128; ++j)
-                                tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], bcol + j * 64, kb * C::BK);
+                                for (int j = 0; j < BN / 128; ++j)
+                                    tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], bcol + j * 64, kb * C::BK);
+                            }
                         } else {
                             const uint32_t lb = mapa_shared(smem_u32(&full[stage]), 0);
                             tma_load_2d_pair(a, &tmA, lb, kb * C::BK, arow);
+                            if (!B_MN) {
+                                tma_load_2d_pair(b, &tmB, lb, kb * C::BK, bcol);
+                            } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 128; ++j)
-                                tma_load_2d_pair(b + j * 64 * C::BK * 2, &tmB, lb, bcol + j * 64, kb * C::BK);
+                                for (int j = 0; j < BN / 128; ++j)
+                                    tma_load_2d_pair(b + j * 64 * C::BK * 2, &tmB, lb, bcol + j * 64, kb * C::BK);
+                            }
                         }
                         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                     }

@@ -21,7 +21,10 @@ RAGGED = [0, 1, 2, 17, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 
 # ----------------------------------------------------------------------------- GEMM (test hook)
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
-@pytest.mark.parametrize("MNK", [(256, 512, 128), (296, 256, 192), (128, 2048, 512), (768, 512, 1024)])
+# (37965, 512, 128): 298 CTA-pair tiles over 74 pairs with a ragged last pair tile -- every CTA
+# walks several tiles (both TMEM accumulators, barrier phase flips)
+@pytest.mark.parametrize("MNK", [(256, 512, 128), (296, 256, 192), (128, 2048, 512), (768, 512, 1024),
+                                 (37965, 512, 128)])
 def test_gemm_bf16_majors(a_mn, b_mn, MNK):
     M, N, K = MNK
     g = torch.Generator().manual_seed(0)
@@ -38,8 +41,10 @@ def test_gemm_bf16_majors(a_mn, b_mn, MNK):
     assert rel_inf(to_np(out), ref.numpy()) < (1e-5 if a_mn else 8e-3)
 
 
-def test_gemm_bf16_silu_and_residual_epilogues():
-    M, N, K = 200, 512, 256
+@pytest.mark.parametrize("b_mn", [True, False])
+@pytest.mark.parametrize("M", [200, 20000])
+def test_gemm_bf16_silu_and_residual_epilogues(b_mn, M):
+    N, K = 512, 256
     g = torch.Generator().manual_seed(1)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = (torch.randn(K, N, generator=g) / 16).bfloat16()
@@ -49,12 +54,13 @@ def test_gemm_bf16_silu_and_residual_epilogues():
     s = torch.sigmoid(h)
     out0 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     out1 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    U.test_gemm(A.cuda(), B.cuda(), False, True, 1, M, N, K, bias=bias.cuda(), out0=out0, out1=out1)
+    U.test_gemm(A.cuda(), (B if b_mn else B.t()).contiguous().cuda(), False, b_mn, 1, M, N, K, bias=bias.cuda(),
+                out0=out0, out1=out1)
     torch.cuda.synchronize()
     assert rel_inf(to_np(out0), (h * s).numpy()) < 8e-3
     assert rel_inf(to_np(out1), (s * (1 + h * (1 - s))).numpy()) < 8e-3
-    out, _ = U.test_gemm(A.cuda(), B.t().contiguous().cuda(), False, False, 0, M, N, K, bias=bias.cuda(),
-                         resid=R.cuda())
+    out, _ = U.test_gemm(A.cuda(), (B if b_mn else B.t()).contiguous().cuda(), False, b_mn, 0, M, N, K,
+                         bias=bias.cuda(), resid=R.cuda())
     torch.cuda.synchronize()
     assert rel_inf(to_np(out), (h + R.double()).numpy()) < 8e-3
 
