@@ -444,3 +444,133 @@ extern "C" uh_status uh_test_gemm(int M, int N, int K, const void* A, int64_t ld
     g.epi = epi; g.out0 = out0; g.ld0 = ld0; g.out1 = out1; g.ld1 = ld1; g.bias = bias; g.resid = resid; g.ldr = ldr;
     return gemm_run(g, dtype, (cudaStream_t)stream);
 }
+
+// ================================================================== NEXT-2: FP8 projections (uhstu_fp8.h)
+#include "../../include/uhstu_fp8.h"
+
+namespace {
+uh_status check_codes_ld(int64_t ld, int64_t width, const char* what) {
+    if (ld < width) return uh::fail(UH_ERR_DIM, std::string(what) + ": row stride smaller than the row width");
+    if (ld % 16) return uh::fail(UH_ERR_ALIGNMENT, std::string(what) + ": code row stride not a multiple of 16 bytes");
+    return UH_OK;
+}
+uh_status check_f32(const void* p, const char* what) {
+    if (!p) return uh::fail(UH_ERR_NULL, std::string(what) + " is NULL");
+    if (reinterpret_cast<uintptr_t>(p) % 4) return uh::fail(UH_ERR_ALIGNMENT, std::string(what) + " not 4-byte aligned");
+    return UH_OK;
+}
+}  // namespace
+
+extern "C" uh_status uh_ln_fwd_fp8(int64_t T, int d, const void* x, int64_t ldx, const float* w, const float* b,
+                                   float eps, uint8_t* q, int64_t ldq, float* scale, float* mean, float* rstd,
+                                   void* stream) {
+    using namespace uh;
+    if (T < 0 || d <= 0 || d % 8 || d > 2048) return fail(UH_ERR_DIM, "ln_fwd_fp8: T >= 0, 0 < d <= 2048, d % 8 == 0");
+    if (T == 0) return UH_OK;
+    UH_TRY(check_ptr(x, "x")); UH_TRY(check_ptr(w, "w")); UH_TRY(check_ptr(b, "b")); UH_TRY(check_ptr(q, "q"));
+    UH_TRY(check_f32(scale, "scale"));
+    UH_TRY(check_ld(ldx, d, UH_BF16, "ldx")); UH_TRY(check_codes_ld(ldq, d, "ldq"));
+    return ln_fwd_fp8(T, d, x, ldx, w, b, eps, q, ldq, scale, mean, rstd, (cudaStream_t)stream);
+}
+
+extern "C" uh_status uh_gated_norm_fwd_fp8(int64_t T, int d, const void* A, int64_t lda, const void* U, int64_t ldu,
+                                           const float* w, const float* b, float eps, uint8_t* q, int64_t ldq,
+                                           float* scale, float* mean, float* rstd, void* stream) {
+    using namespace uh;
+    if (T < 0 || d <= 0 || d % 8 || d > 2048) return fail(UH_ERR_DIM, "gated_norm_fwd_fp8: T >= 0, 0 < d <= 2048, d % 8 == 0");
+    if (T == 0) return UH_OK;
+    UH_TRY(check_ptr(A, "A")); UH_TRY(check_ptr(U, "U")); UH_TRY(check_ptr(w, "w")); UH_TRY(check_ptr(b, "b"));
+    UH_TRY(check_ptr(q, "q")); UH_TRY(check_f32(scale, "scale"));
+    UH_TRY(check_ld(lda, d, UH_BF16, "lda")); UH_TRY(check_ld(ldu, d, UH_BF16, "ldu"));
+    UH_TRY(check_codes_ld(ldq, d, "ldq"));
+    return gated_norm_fwd_fp8(T, d, A, lda, U, ldu, w, b, eps, q, ldq, scale, mean, rstd, (cudaStream_t)stream);
+}
+
+extern "C" uh_status uh_quant_weight_fp8(int K, int N, const void* W, int64_t ldw, uint8_t* qt, int64_t ldq,
+                                         float* scale, void* stream) {
+    using namespace uh;
+    if (K < 0 || N < 0) return fail(UH_ERR_DIM, "quant_weight_fp8: K, N >= 0");
+    if (K == 0 || N == 0) return UH_OK;
+    UH_TRY(check_ptr(W, "W")); UH_TRY(check_ptr(qt, "qt")); UH_TRY(check_f32(scale, "scale"));
+    UH_TRY(check_ld(ldw, N, UH_BF16, "ldw")); UH_TRY(check_codes_ld(ldq, K, "ldq"));
+    return quant_weight_fp8(K, N, W, ldw, qt, ldq, scale, (cudaStream_t)stream);
+}
+
+extern "C" uh_status uh_gemm_fp8(int M, int N, int K, const uint8_t* qa, int64_t lda, const float* sa,
+                                 const uint8_t* qb, int64_t ldb, const float* sb, int epi, void* out, int64_t ldo,
+                                 const float* bias, const void* resid, int64_t ldr, void* stream) {
+    using namespace uh;
+    if (M < 0 || N < 0 || K < 0) return fail(UH_ERR_DIM, "gemm_fp8: M, N, K >= 0");
+    if (epi != 0 && epi != 1) return fail(UH_ERR_DOMAIN, "gemm_fp8: epi must be 0 (bf16 + bias + resid) or 1 (silu)");
+    if (epi == 1 && resid) return fail(UH_ERR_DOMAIN, "gemm_fp8: the SiLU epilogue takes no residual");
+    if (M == 0 || N == 0) return UH_OK;
+    UH_TRY(check_ptr(qa, "qa")); UH_TRY(check_ptr(qb, "qb")); UH_TRY(check_ptr(out, "out"));
+    UH_TRY(check_f32(sa, "sa")); UH_TRY(check_f32(sb, "sb"));
+    UH_TRY(check_codes_ld(lda, K, "lda")); UH_TRY(check_codes_ld(ldb, K, "ldb"));
+    UH_TRY(check_ld(ldo, N, UH_BF16, "ldo"));
+    if (resid) { UH_TRY(check_ptr(resid, "resid")); UH_TRY(check_ld(ldr, N, UH_BF16, "ldr")); }
+    GemmDesc g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = qa; g.lda = lda; g.B = qb; g.ldb = ldb;
+    g.epi = epi == 1 ? EPI_SILU : EPI_BF16;
+    g.out0 = out; g.ld0 = ldo; g.bias = bias; g.resid = resid; g.ldr = ldr;
+    return gemm_fp8_run(g, sa, sb, (cudaStream_t)stream);
+}
+
+extern "C" uh_status uh_layer_fwd_fp8(const uh_jagged* jag, uh_mask m, const uh_layer_params* p,
+                                      const uh_fp8_weights* qw, const void* x, void* out, uh_layer_saved* saved,
+                                      void* ws, size_t ws_bytes, void* stream) {
+    using namespace uh;
+    const uh_dtype dtype = UH_BF16;
+    UH_TRY(check_layer(jag, m, p, dtype));
+    if (!qw || !qw->w1t || !qw->s1 || !qw->w2t || !qw->s2) return fail(UH_ERR_NULL, "fp8 weights NULL");
+    const int64_t T = jag->total_tokens;
+    if (T == 0) return UH_OK;
+    UH_TRY(check_ptr(x, "x")); UH_TRY(check_ptr(out, "out"));
+    if (saved) {
+        UH_TRY(check_ptr(saved->attn, "saved.attn"));
+        if (!saved->ln1_mean || !saved->ln1_rstd || !saved->ln2_mean || !saved->ln2_rstd)
+            return fail(UH_ERR_NULL, "saved statistics NULL");
+    }
+    const int d = p->attn.num_heads * p->attn.head_dim;
+    if (d % 128) return fail(UH_ERR_UNSUPPORTED, "fp8 layer needs d % 128 == 0");
+    const LayerWs w = layer_ws(jag, m, p, dtype, 0);
+    if (!ws || ws_bytes < w.total) return fail(UH_ERR_WORKSPACE, "workspace too small: need " + std::to_string(w.total));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t es = 2;
+    uint8_t* W = (uint8_t*)ws;
+    uint8_t* codes = W + w.xh;            // [T][d] E4M3 (x^, then Y): fits the bf16 x^ slot
+    float* rscale = (float*)(W + w.ybuf); // [T] row scales: fits the bf16 Y slot
+    uint8_t* uvqk = W + w.uvqk;
+    void* A = saved ? saved->attn : (void*)(W + w.attn_buf);
+    float* st4 = (float*)(W + w.stats);
+    float* mu1 = saved ? saved->ln1_mean : st4;
+    float* rs1 = saved ? saved->ln1_rstd : st4 + T;
+    float* mu2 = saved ? saved->ln2_mean : st4 + 2 * T;
+    float* rs2 = saved ? saved->ln2_rstd : st4 + 3 * T;
+
+    // F1 + quant: codes(x^), s_x                                           (Eq. 1)
+    UH_TRY(ln_fwd_fp8(T, d, x, d, p->ln1_w, p->ln1_b, p->eps, codes, d, rscale, mu1, rs1, st));
+    // F2: UVQK = silu(s_x (q_x q_W1^T) s_W1 + b1)                          (Eq. 2)
+    GemmDesc g1;
+    g1.M = (int)T; g1.N = 4 * d; g1.K = d;
+    g1.A = codes; g1.lda = d; g1.B = qw->w1t; g1.ldb = d;
+    g1.epi = EPI_SILU; g1.out0 = uvqk; g1.ld0 = 4 * d; g1.bias = p->b1;
+    UH_TRY(gemm_fp8_run(g1, rscale, qw->s1, st));
+    // F3-F5: A = attention(Q, K, V), bf16                                  (Eq. 3)
+    AttnCall c{};
+    c.jag = jag; c.mask = m; c.desc = &p->attn;
+    c.q = uvqk + 2 * d * es; c.k = uvqk + 3 * d * es; c.v = uvqk + 1 * d * es; c.ld_qkv = 4 * d;
+    c.out = A; c.ld_out = d;
+    c.ws = W + w.attn_ws; c.ws_bytes = w.total - w.attn_ws; c.st = st;
+    UH_TRY(attn_fwd_run(c, dtype));
+    // F6 + quant: codes(Y), s_Y with Y = LN(A) (.) U                      (Eq. 4 inner)
+    UH_TRY(gated_norm_fwd_fp8(T, d, A, d, uvqk, 4 * d, p->ln2_w, p->ln2_b, p->eps, codes, d, rscale, mu2, rs2, st));
+    // F7: out = s_Y (q_Y q_W2^T) s_W2 + b2 + x                             (Eqs. 4-5)
+    GemmDesc g2;
+    g2.M = (int)T; g2.N = d; g2.K = d;
+    g2.A = codes; g2.lda = d; g2.B = qw->w2t; g2.ldb = d;
+    g2.epi = EPI_BF16; g2.out0 = out; g2.ld0 = d; g2.bias = p->b2; g2.resid = x; g2.ldr = d;
+    UH_TRY(gemm_fp8_run(g2, rscale, qw->s2, st));
+    return UH_OK;
+}

@@ -157,6 +157,51 @@ static uh_status launch_sm100(const GemmDesc& g, cudaStream_t st) {
     return UH_OK;
 }
 
+// ============================================================== E4M3 tcgen05 (NEXT-2)
+template <int BN, int EPI>
+static uh_status launch_fp8(const GemmDesc& g, const float* sa, const float* sb, cudaStream_t st) {
+    using C = GemmCfg<BN, 1, EPI, 1>;
+    CUtensorMap ta, tb, to0, to1;
+    UH_TRY(make_tmap_u8(&ta, g.A, g.K, g.M, g.lda, 128, C::BM));    // [M][K] codes, 128-byte K rows
+    UH_TRY(make_tmap_u8(&tb, g.B, g.K, g.N, g.ldb, 128, BN));       // B^T [N][K]
+    UH_TRY(make_tmap_bf16(&to0, g.out0, g.N, g.M, g.ld0, 32, 32, 64));
+    to1 = to0;
+    if (g.out1) UH_TRY(make_tmap_bf16(&to1, g.out1, g.N, g.M, g.ld1, 32, 32, 64));
+    GemmArgs a;
+    a.M = g.M; a.N = g.N; a.K = g.K;
+    a.m_tiles = (g.M + C::BM - 1) / C::BM;
+    a.n_tiles = (g.N + BN - 1) / BN;
+    a.kb_per_split = (g.K + 127) / 128;
+    a.k_splits = 1;
+    a.out0 = g.out0; a.ld0 = g.ld0; a.out1 = g.out1; a.ld1 = g.ld1;
+    a.bias = g.bias; a.resid = (const __nv_bfloat16*)g.resid; a.ldr = g.ldr;
+    a.colsum = nullptr;
+    a.scale_a = sa; a.scale_b = sb;
+    const int total = a.m_tiles * a.n_tiles;
+    auto kern = gemm_bf16_sm100<BN, false, false, EPI, 1, 1, true>;
+    UH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    kern<<<std::min(total, num_sms()), 384, C::SMEM, st>>>(ta, tb, to0, to1, a);
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status gemm_fp8_run(const GemmDesc& g, const float* sa, const float* sb, cudaStream_t st) {
+    if (g.M == 0 || g.N == 0) return UH_OK;
+    if (g.K <= 0 || g.K % 128) return fail(UH_ERR_UNSUPPORTED, "fp8 gemm needs K % 128 == 0");
+    if (g.N % 128) return fail(UH_ERR_UNSUPPORTED, "fp8 gemm needs N % 128 == 0");
+    if (g.a_mn || g.b_mn) return fail(UH_ERR_UNSUPPORTED, "fp8 gemm operands are K-major");
+    if (g.epi == EPI_SILU) {
+        if (g.N % 256 == 0) return launch_fp8<256, EPI_SILU>(g, sa, sb, st);
+        return launch_fp8<128, EPI_SILU>(g, sa, sb, st);
+    }
+    if (g.epi == EPI_BF16) {
+        if (g.N % 256 == 0) return launch_fp8<256, EPI_BF16>(g, sa, sb, st);
+        return launch_fp8<128, EPI_BF16>(g, sa, sb, st);
+    }
+    return fail(UH_ERR_UNSUPPORTED, "fp8 gemm epilogue");
+}
+
 uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
     if (g.M == 0 || g.N == 0) return UH_OK;
     if (g.K == 0) return g.epi == EPI_F32 ? UH_OK : fail(UH_ERR_UNSUPPORTED, "gemm with K == 0");
@@ -173,9 +218,10 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         return fail(UH_ERR_UNSUPPORTED, "gemm EPI_F32 with mixed majors");
     }
     if (g.a_mn) return fail(UH_ERR_UNSUPPORTED, "gemm bf16-out with MN-major A");
-    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A projections; UH_GEMM_PAIR=0
-    // disables them, =1 keeps them to MN-major B (f1, f2), otherwise both B majors (also dY)
-    static const int pair_mode = [] { const char* e = getenv("UH_GEMM_PAIR"); return e ? atoi(e) : 2; }();
+    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A projections; UH_GEMM_PAIR=1
+    // enables them for MN-major B (f1, f2), =2 for both B majors (also dY); unset / 0: off
+    const char* pe = getenv("UH_GEMM_PAIR");   // read per call (measured equal to single CTAs: off by default)
+    const int pair_mode = pe ? atoi(pe) : 0;
     const bool pair = wide && (pair_mode >= 2 || (pair_mode == 1 && g.b_mn));
     if (g.epi == EPI_SILU) {
         if (pair) {

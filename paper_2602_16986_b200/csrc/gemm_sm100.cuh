@@ -32,6 +32,8 @@ struct GemmArgs {
     const float* bias;
     const __nv_bfloat16* resid; int64_t ldr;
     float* colsum;      // EPI_F32, 256-wide MN-major B: += column sums of B (the bias gradient), or null
+    const float* scale_a = nullptr;   // F8: per-row scales of A [M]
+    const float* scale_b = nullptr;   // F8: per-column scales of B [N]
 };
 
 // MSUB row sub-tiles of 128 share each B k-block (tile BM = 128 MSUB): for the long-K split-K
@@ -55,12 +57,16 @@ struct GemmCfg {
     static constexpr int TMEM_COLS = NACC * MSUB * BN <= 256 ? 256 : 512;
 };
 
-template <int BN, bool A_MN, bool B_MN, int EPI, int MSUB = 1, int CG = 1>
+// F8 (NEXT-2): E4M3 A and B^T, both K-major, kind::f8f6f4; a K block is 128 elements (the same
+// 128-byte rows, swizzle and descriptors as bf16's 64), the epilogue applies diag(sa) . diag(sb)
+template <int BN, bool A_MN, bool B_MN, int EPI, int MSUB = 1, int CG = 1, bool F8 = false>
 __global__ void __launch_bounds__(384, 1)
 gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1, GemmArgs g) {
     using C = GemmCfg<BN, MSUB, EPI, CG>;
     static_assert(CG == 1 || (MSUB == 1 && !A_MN && BN == 256 && EPI != EPI_F32), "CTA-pair GEMM shape");
+    static_assert(!F8 || (!A_MN && !B_MN && MSUB == 1 && CG == 1 && EPI != EPI_F32), "FP8 GEMM shape");
+    constexpr int KE = F8 ? 128 : C::BK;   // K elements per k-block
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -103,7 +109,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         nt = r - mt * g.n_tiles;
     };
     auto kb_range = [&](int ks, int& kb0, int& kb1) {
-        int nkb = (g.K + C::BK - 1) / C::BK;
+        int nkb = (g.K + KE - 1) / KE;
         kb0 = ks * g.kb_per_split;
         kb1 = min(nkb, kb0 + g.kb_per_split);
     };
@@ -124,23 +130,23 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         const int arow = mt * 256 + (int)rank * 128, bcol = nt * BN + (int)rank * (BN / 2);
                         if (rank == 0) {
                             mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-                            tma_load_2d(a, &tmA, &full[stage], kb * C::BK, arow);
+                            tma_load_2d(a, &tmA, &full[stage], kb * KE, arow);
                             if (!B_MN) {
-                                tma_load_2d(b, &tmB, &full[stage], kb * C::BK, bcol);
+                                tma_load_2d(b, &tmB, &full[stage], kb * KE, bcol);
                             } else {
 #pragma unroll
                                 for (int j = 0; j < BN / 128; ++j)
-                                    tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], bcol + j * 64, kb * C::BK);
+                                    tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], bcol + j * 64, kb * KE);
                             }
                         } else {
                             const uint32_t lb = mapa_shared(smem_u32(&full[stage]), 0);
-                            tma_load_2d_pair(a, &tmA, lb, kb * C::BK, arow);
+                            tma_load_2d_pair(a, &tmA, lb, kb * KE, arow);
                             if (!B_MN) {
-                                tma_load_2d_pair(b, &tmB, lb, kb * C::BK, bcol);
+                                tma_load_2d_pair(b, &tmB, lb, kb * KE, bcol);
                             } else {
 #pragma unroll
                                 for (int j = 0; j < BN / 128; ++j)
-                                    tma_load_2d_pair(b + j * 64 * C::BK * 2, &tmB, lb, bcol + j * 64, kb * C::BK);
+                                    tma_load_2d_pair(b + j * 64 * C::BK * 2, &tmB, lb, bcol + j * 64, kb * KE);
                             }
                         }
                         if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -153,18 +159,18 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     uint8_t* a = sA + stage * C::A_BYTES;
                     uint8_t* b = sB + stage * C::B_BYTES;
                     if (!A_MN) {
-                        tma_load_2d(a, &tmA, &full[stage], kb * C::BK, mt * C::BM);
+                        tma_load_2d(a, &tmA, &full[stage], kb * KE, mt * C::BM);
                     } else {
 #pragma unroll
                         for (int j = 0; j < C::BM / 64; ++j)
-                            tma_load_2d(a + j * 64 * C::BK * 2, &tmA, &full[stage], mt * C::BM + j * 64, kb * C::BK);
+                            tma_load_2d(a + j * 64 * C::BK * 2, &tmA, &full[stage], mt * C::BM + j * 64, kb * KE);
                     }
                     if (!B_MN) {
-                        tma_load_2d(b, &tmB, &full[stage], kb * C::BK, nt * BN);
+                        tma_load_2d(b, &tmB, &full[stage], kb * KE, nt * BN);
                     } else {
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
-                            tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], nt * BN + j * 64, kb * C::BK);
+                            tma_load_2d(b + j * 64 * C::BK * 2, &tmB, &full[stage], nt * BN + j * 64, kb * KE);
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -172,7 +178,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else if (warp == 1 && rank == 0) {
         // ------------------------------------------------ MMA issuer (CTA pairs: the leader, M = 256)
-        constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
+        constexpr uint32_t idesc = F8 ? make_idesc_e4m3(128, BN) : make_idesc_bf16(128 * CG, BN, A_MN, B_MN);
         int stage = 0; uint32_t phase = 0;
         int it = 0;
         for (int t = t_first; t < total; t += t_step, ++it) {
@@ -203,6 +209,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                             uint64_t ad = A_MN ? make_sw128_desc(a0 + ms * 16384 + k * 2048, 64 * C::BK * 2, 1024)
                                                : make_sw128_desc(a0 + ms * 16384 + k * 32, 16, 1024);
                             if (CG == 2) umma_ss_pair(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                            else if (F8) umma_ss_e4m3(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                             else umma_ss(d_tmem + ms * BN, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                         }
                     }
@@ -226,6 +233,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int row_in_tile = wq * 32 + (int)lane_id();
         int it = 0;
         int cs_stage = 0; uint32_t cs_phase = 0;   // B-stage sequence (mirrors the MMA issuer's)
+        uint32_t n_chunk = 0;                      // TMA-store chunks this warp has staged
         const int row_base = CG == 2 ? (int)rank * 128 : 0;   // this CTA's half of a pair tile
         for (int t = t_first; t < total; t += t_step, ++it) {
             int mt, nt, ks;
@@ -282,6 +290,12 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                 const int cb = nt * BN + wg * (BN / 2) + 32 * q + (int)lane_id();
                 bl[q] = (EPI != EPI_F32 && g.bias && cb < g.N) ? __ldg(g.bias + cb) * (EPI == EPI_SILU ? 0.5f : 1.0f) : 0.f;
             }
+            float sbl[F8 ? NCH : 1];   // F8: this warp's column scales, one per lane per chunk (x 1/2 for SiLU's h/2)
+#pragma unroll
+            for (int q = 0; q < (F8 ? NCH : 1); ++q) {
+                const int cb = nt * BN + wg * (BN / 2) + 32 * q + (int)lane_id();
+                sbl[q] = (F8 && cb < g.N) ? __ldg(g.scale_b + cb) * (EPI == EPI_SILU ? 0.5f : 1.0f) : 0.f;
+            }
             const int acc = C::NACC == 2 ? (it & 1) : 0;
             mbar_wait(&tfull[acc], C::NACC == 2 ? ((it >> 1) & 1) : (it & 1));
             tc_fence_after();
@@ -289,6 +303,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             for (int ms = 0; ms < MSUB; ++ms) {
             const int row = mt * C::BM * CG + row_base + ms * 128 + row_in_tile;
             const bool row_ok = row < g.M;
+            const float sa_row = (F8 && row_ok) ? __ldg(g.scale_a + row) : 0.f;
 #pragma unroll 1
             for (int c0 = wg * (BN / 2); c0 < (wg + 1) * (BN / 2); c0 += 32) {
                 float v[32];
@@ -321,6 +336,14 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
                         for (int j = 0; j < 32; ++j) hb[j] = __shfl_sync(0xffffffffu, bq, j);
                     }
+                    if (F8) {   // acc x sa x sb: the SiLU's 1/2 rides in sb, so the epilogues below see 1/2 -> 1
+                        const int q = (c0 - wg * (BN / 2)) >> 5;
+                        float sq = sbl[0];
+#pragma unroll
+                        for (int qq = 1; qq < (F8 ? NCH : 1); ++qq) sq = q == qq ? sbl[qq] : sq;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] *= sa_row * __shfl_sync(0xffffffffu, sq, j);
+                    }
                     uint32_t o0[16], o1[16];
                     if (EPI == EPI_BF16) {
 #pragma unroll
@@ -343,7 +366,7 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         const uint64_t half2 = f2_pack(0.5f, 0.5f), one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            const uint64_t H = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), half2, f2_pack(hb[2 * i], hb[2 * i + 1]));
+                            const uint64_t H = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), F8 ? one2 : half2, f2_pack(hb[2 * i], hb[2 * i + 1]));
                             const float2 hh = f2_unpack(H);
                             const uint64_t T = f2_pack(tanh_approx(hh.x), tanh_approx(hh.y));
                             const float2 sv = f2_unpack(ffma2(H, T, H));
@@ -356,9 +379,14 @@ gemm_bf16_sm100(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     }
                     // rows of this warp -> its 64B-swizzled 32x32 staging boxes -> TMA stores
                     // (coalesced; rows / columns beyond M, N are clipped by the tensor map)
-                    uint8_t* box0 = stg + (warp - 4) * 4096;
-                    uint8_t* box1 = box0 + 2048;
-                    if (lane_id() == 0) bulk_wait_read0();   // the previous stores have read the boxes
+                    // one output: the two 2 KB boxes alternate chunk by chunk, so a chunk's staging
+                    // overlaps the previous chunk's TMA read (wait for all but the newest group);
+                    // two outputs: box0 / box1 per chunk, all previous stores read first
+                    const bool dbuf = !(EPI == EPI_SILU && g.out1);
+                    uint8_t* box0 = stg + (warp - 4) * 4096 + (dbuf && (n_chunk & 1) ? 2048 : 0);
+                    uint8_t* box1 = stg + (warp - 4) * 4096 + 2048;
+                    ++n_chunk;
+                    if (lane_id() == 0) { if (dbuf) bulk_wait_read1(); else bulk_wait_read0(); }
                     __syncwarp();
                     const int r = lane_id();
 #pragma unroll

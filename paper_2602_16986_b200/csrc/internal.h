@@ -29,6 +29,9 @@ uh_status cuda_fail(cudaError_t e, const char* where);
 // bf16 2-D tensor map, 128-byte swizzle, box {box_inner, box_outer}
 uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                          uint32_t box_inner, uint32_t box_outer, int swizzle_bytes = 128);
+// 8-bit (E4M3) 2-D tensor map, 128-byte swizzle; ld in bytes
+uh_status make_tmap_u8(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                       uint32_t box_inner, uint32_t box_outer);
 // fp32 2-D tensor map, no swizzle (TMA reduce-add targets)
 uh_status make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                         uint32_t box_inner, uint32_t box_outer);
@@ -51,6 +54,9 @@ struct GemmDesc {
     float* colsum = nullptr;   // EPI_F32 only: += column sums of B (fused bias gradient)
 };
 uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st);
+// NEXT-2: D = diag(sa) (A B) diag(sb) (+ bias)(+ resid) with A [M,K] and B^T [N,K] E4M3, K-major,
+// epi EPI_BF16 or EPI_SILU (g.A / g.B the codes, lda / ldb in bytes); K % 128 == 0, N % 128 == 0
+uh_status gemm_fp8_run(const GemmDesc& g, const float* sa, const float* sb, cudaStream_t st);
 
 // ------------------------------------------------------------------ norms (norm.cu)
 // x^ = LN(x) with stats out (mean/rstd may be null)
@@ -63,6 +69,15 @@ uh_status ln_apply(uh_dtype dt, int64_t T, int d, const void* x, int64_t ldx, co
 uh_status gated_norm_fwd(uh_dtype dt, int64_t T, int d, const void* A, int64_t lda, const void* U, int64_t ldu,
                          const float* w, const float* b, float eps, void* Y, int64_t ldy, float* mean, float* rstd,
                          cudaStream_t st);
+// NEXT-2: LN / gated norm with the row-wise E4M3 quantisation fused (bf16 in, codes [T,d] + scale [T])
+uh_status ln_fwd_fp8(int64_t T, int d, const void* x, int64_t ldx, const float* w, const float* b, float eps,
+                     uint8_t* q, int64_t ldq, float* scale, float* mean, float* rstd, cudaStream_t st);
+uh_status gated_norm_fwd_fp8(int64_t T, int d, const void* A, int64_t lda, const void* U, int64_t ldu,
+                             const float* w, const float* b, float eps, uint8_t* q, int64_t ldq, float* scale,
+                             float* mean, float* rstd, cudaStream_t st);
+// W [K,N] bf16 -> W^T codes [N,K] + per-column scales [N]
+uh_status quant_weight_fp8(int K, int N, const void* W, int64_t ldw, uint8_t* qt, int64_t ldq, float* scale,
+                           cudaStream_t st);
 // gated norm backward: dA, dH_U = (dY (.) A^) (.) G_U, Y (recomputed), dw, db (+=)
 uh_status gated_norm_bwd(uh_dtype dt, int64_t T, int d, const void* dY, int64_t lddy, const void* A, int64_t lda,
                          const void* U, int64_t ldu, const void* GU, int64_t ldg, const float* w, const float* b,

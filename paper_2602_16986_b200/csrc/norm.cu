@@ -177,6 +177,174 @@ __global__ void __launch_bounds__(256) gated_fwd_k(int64_t nrows, int d, const T
     }
 }
 
+// ------------------------------------------------------------------ NEXT-2: norms fused with row-wise E4M3
+// quantisation (Fig. fp8: "fuse the scaling/quantization steps with the preceding kernels").
+// The row's normalised values stay in registers (fp32); amax by warp max; s = amax / 448,
+// code = E4M3_rn_sat(v * (448 / amax)) in fp32 (readings R18, R19); an all-zero row gets s = 1.
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+template <int CPL>
+__device__ __forceinline__ void quant_row_store(float (&o)[CPL][8], int lane, int nch, uint8_t* q, float* scale,
+                                                int64_t row) {
+    float am = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+        if (lane + 32 * c < nch)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) am = fmaxf(am, fabsf(o[c][e]));
+    am = warp_max(am);
+    const float inv = am > 0.f ? __fdiv_rn(448.f, am) : 1.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nch) {
+            uint2 pk;
+            pk.x = (uint32_t)cvt_e4m3x2(__fmul_rn(o[c][0], inv), __fmul_rn(o[c][1], inv))
+                 | ((uint32_t)cvt_e4m3x2(__fmul_rn(o[c][2], inv), __fmul_rn(o[c][3], inv)) << 16);
+            pk.y = (uint32_t)cvt_e4m3x2(__fmul_rn(o[c][4], inv), __fmul_rn(o[c][5], inv))
+                 | ((uint32_t)cvt_e4m3x2(__fmul_rn(o[c][6], inv), __fmul_rn(o[c][7], inv)) << 16);
+            *reinterpret_cast<uint2*>(q + ch * 8) = pk;
+        }
+    }
+    if (lane == 0) scale[row] = am > 0.f ? __fdiv_rn(am, 448.f) : 1.f;
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(256) ln_fwd_fp8_k(int64_t nrows, int d, const __nv_bfloat16* __restrict__ x,
+                                                    int64_t ldx, const float* __restrict__ w,
+                                                    const float* __restrict__ b, float eps, uint8_t* __restrict__ q,
+                                                    int64_t ldq, float* __restrict__ scale, float* mean, float* rstd) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    const int nch = d / 8;
+    float v[CPL][8];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nch) {
+            Vec<__nv_bfloat16>::load(x + row * ldx + ch * 8, v[c]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s += v[c][e];
+        }
+    }
+    const float mu = warp_sum(s) / d;
+    float qq = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+        if (lane + 32 * c < nch)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { float t = v[c][e] - mu; qq += t * t; }
+    const float rs = rsqrtf(warp_sum(qq) / d + eps);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nch) {
+            float wv[8], bv[8];
+            load4f(w + ch * 8, wv); load4f(w + ch * 8 + 4, wv + 4);
+            load4f(b + ch * 8, bv); load4f(b + ch * 8 + 4, bv + 4);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[c][e] = (v[c][e] - mu) * rs * wv[e] + bv[e];
+        }
+    }
+    quant_row_store<CPL>(v, lane, nch, q + row * ldq, scale, row);
+    if (lane == 0) {
+        if (mean) mean[row] = mu;
+        if (rstd) rstd[row] = rs;
+    }
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(256) gated_fwd_fp8_k(int64_t nrows, int d, const __nv_bfloat16* __restrict__ A,
+                                                       int64_t lda, const __nv_bfloat16* __restrict__ U, int64_t ldu,
+                                                       const float* __restrict__ w, const float* __restrict__ b,
+                                                       float eps, uint8_t* __restrict__ q, int64_t ldq,
+                                                       float* __restrict__ scale, float* mean, float* rstd) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    const int nch = d / 8;
+    float v[CPL][8], u[CPL][8];
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nch) {
+            Vec<__nv_bfloat16>::load(A + row * lda + ch * 8, v[c]);
+            Vec<__nv_bfloat16>::load(U + row * ldu + ch * 8, u[c]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s += v[c][e];
+        }
+    }
+    const float mu = warp_sum(s) / d;
+    float qq = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+        if (lane + 32 * c < nch)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { float t = v[c][e] - mu; qq += t * t; }
+    const float rs = rsqrtf(warp_sum(qq) / d + eps);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        const int ch = lane + 32 * c;
+        if (ch < nch) {
+            float wv[8], bv[8];
+            load4f(w + ch * 8, wv); load4f(w + ch * 8 + 4, wv + 4);
+            load4f(b + ch * 8, bv); load4f(b + ch * 8 + 4, bv + 4);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[c][e] = ((v[c][e] - mu) * rs * wv[e] + bv[e]) * u[c][e];
+        }
+    }
+    quant_row_store<CPL>(v, lane, nch, q + row * ldq, scale, row);
+    if (lane == 0) {
+        if (mean) mean[row] = mu;
+        if (rstd) rstd[row] = rs;
+    }
+}
+
+// weight W [K, N] (bf16, row stride ldw) -> W^T codes [N, K] (K-major, row stride ldq bytes) and one scale
+// per output column (R18).  Block = 32 columns x 8 row groups; the transposed codes are written
+// through a shared-memory tile so both the reads and the writes are coalesced.
+__global__ void __launch_bounds__(256) quant_weight_fp8_k(int K, int N, const __nv_bfloat16* __restrict__ W,
+                                                          int64_t ldw, uint8_t* __restrict__ qt, int64_t ldq,
+                                                          float* __restrict__ scale) {
+    __shared__ float red[8][33];
+    __shared__ uint8_t tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int n = blockIdx.x * 32 + tx;
+    float am = 0.f;
+    if (n < N)
+        for (int k = ty; k < K; k += 8) am = fmaxf(am, fabsf(__bfloat162float(W[(int64_t)k * ldw + n])));
+    red[ty][tx] = am;
+    __syncthreads();
+    if (ty == 0) {
+        for (int i = 1; i < 8; ++i) am = fmaxf(am, red[i][tx]);
+        red[0][tx] = am;
+        if (n < N) scale[n] = am > 0.f ? __fdiv_rn(am, 448.f) : 1.f;
+    }
+    __syncthreads();
+    const float colmax = red[0][tx];
+    const float inv = colmax > 0.f ? __fdiv_rn(448.f, colmax) : 1.f;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        for (int kk = ty; kk < 32; kk += 8) {   // read rows k0 + kk, column n
+            const int k = k0 + kk;
+            const float v = (n < N && k < K) ? __bfloat162float(W[(int64_t)k * ldw + n]) : 0.f;
+            tile[tx][kk] = (uint8_t)(cvt_e4m3x2(__fmul_rn(v, inv), 0.f) & 0xFF);
+        }
+        __syncthreads();
+        for (int nn = ty; nn < 32; nn += 8) {   // write qt[n0 + nn][k0 + tx]
+            const int n2 = blockIdx.x * 32 + nn, k = k0 + tx;
+            if (n2 < N && k < K) qt[(int64_t)n2 * ldq + k] = tile[nn][tx];
+        }
+        __syncthreads();
+    }
+}
+
 // block-level reduction of per-lane parameter-gradient partials, then one atomic per column
 template <typename T, int CPL>
 __device__ __forceinline__ void flush_param_grads(int d, float (*pw)[Vec<T>::N], float (*pb)[Vec<T>::N], float* dw,
@@ -660,6 +828,39 @@ uh_status gated_norm_fwd(uh_dtype dt, int64_t T_, int d, const void* A, int64_t 
     UH_DT_DISPATCH(dt, UH_CPL_DISPATCH(T, d,
         gated_fwd_k<T, CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const T*)A, lda, (const T*)U, ldu, w, b, eps,
                                                            (T*)Y, ldy, mean, rstd)));
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status ln_fwd_fp8(int64_t T_, int d, const void* x, int64_t ldx, const float* w, const float* b, float eps,
+                     uint8_t* q, int64_t ldq, float* scale, float* mean, float* rstd, cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_CPL_DISPATCH(__nv_bfloat16, d,
+        ln_fwd_fp8_k<CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const __nv_bfloat16*)x, ldx, w, b, eps, q, ldq,
+                                                         scale, mean, rstd));
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status gated_norm_fwd_fp8(int64_t T_, int d, const void* A, int64_t lda, const void* U, int64_t ldu,
+                             const float* w, const float* b, float eps, uint8_t* q, int64_t ldq, float* scale,
+                             float* mean, float* rstd, cudaStream_t st) {
+    if (T_ == 0) return UH_OK;
+    UH_CPL_DISPATCH(__nv_bfloat16, d,
+        gated_fwd_fp8_k<CPL><<<grid_rows(T_), 256, 0, st>>>(T_, d, (const __nv_bfloat16*)A, lda,
+                                                            (const __nv_bfloat16*)U, ldu, w, b, eps, q, ldq, scale,
+                                                            mean, rstd));
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
+}
+
+uh_status quant_weight_fp8(int K, int N, const void* W, int64_t ldw, uint8_t* qt, int64_t ldq, float* scale,
+                           cudaStream_t st) {
+    if (K == 0 || N == 0) return UH_OK;
+    quant_weight_fp8_k<<<(N + 31) / 32, 256, 0, st>>>(K, N, (const __nv_bfloat16*)W, ldw, qt, ldq, scale);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;

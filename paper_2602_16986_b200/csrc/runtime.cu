@@ -58,6 +58,23 @@ uh_status make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint
     return UH_OK;
 }
 
+uh_status make_tmap_u8(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_bytes,
+                       uint32_t box_inner, uint32_t box_outer) {
+    auto enc = get_encode();
+    if (!enc) return fail(UH_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if (outer == 0) outer = 1;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(UH_ERR_CUDA, "cuTensorMapEncodeTiled (u8) failed (code " + std::to_string((int)r) + ")");
+    return UH_OK;
+}
+
 uh_status make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                         uint32_t box_inner, uint32_t box_outer) {
     auto enc = get_encode();

@@ -155,6 +155,7 @@ UH_DEV void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int 
 }
 UH_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 UH_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+UH_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 UH_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // ---------------------------------------------------------------- fences
@@ -278,6 +279,22 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(uint32_t M, uint32_t N, b
          | ((b_mn_major ? 1u : 0u) << 16)  // B major
          | ((N >> 3) << 17)                // N / 8
          | ((M >> 4) << 24);               // M / 16
+}
+
+// Instruction descriptor, kind::f8f6f4: E4M3 A/B (format code 0), fp32 D, dense (NEXT-2).
+__host__ __device__ constexpr uint32_t make_idesc_e4m3(uint32_t M, uint32_t N) {
+    return (1u << 4)                       // D format fp32
+         | ((N >> 3) << 17)                // N / 8
+         | ((M >> 4) << 24);               // M / 16
+}
+// D (+)= A * B with E4M3 operands, both K-major in 128B-swizzled shared memory (K = 32 per MMA)
+UH_DEV void umma_ss_e4m3(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;}"
+                 ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// two fp32 -> packed E4M3x2 (lo in the low byte), round to nearest even, saturating at +-448
+UH_DEV uint16_t cvt_e4m3x2(float lo, float hi) {
+    uint16_t r; asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo)); return r;
 }
 
 // ---------------------------------------------------------------- misc math

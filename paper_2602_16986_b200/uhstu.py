@@ -63,6 +63,11 @@ class LayerGrads(ctypes.Structure):
                 ("ln1_w", "ln1_b", "w1", "b1", "ln2_w", "ln2_b", "w2", "b2", "pos_bias", "time_bias")]
 
 
+class Fp8Weights(ctypes.Structure):
+    """uh_fp8_weights (include/uhstu_fp8.h)."""
+    _fields_ = [("w1t", ctypes.c_void_p), ("s1", ctypes.c_void_p), ("w2t", ctypes.c_void_p), ("s2", ctypes.c_void_p)]
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -100,6 +105,19 @@ def lib():
                                    ctypes.c_int, ctypes.c_int, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp]
         L.uh_test_gemm.restype = ctypes.c_int
         L.uh_test_launch_count.restype = ctypes.c_longlong
+        # NEXT-2: FP8 projections (include/uhstu_fp8.h)
+        u8p = ctypes.c_void_p
+        L.uh_ln_fwd_fp8.argtypes = [i64, ctypes.c_int, vp, i64, vp, vp, ctypes.c_float, u8p, i64, vp, vp, vp, vp]
+        L.uh_gated_norm_fwd_fp8.argtypes = [i64, ctypes.c_int, vp, i64, vp, i64, vp, vp, ctypes.c_float, u8p, i64,
+                                            vp, vp, vp, vp]
+        L.uh_quant_weight_fp8.argtypes = [ctypes.c_int, ctypes.c_int, vp, i64, u8p, i64, vp, vp]
+        L.uh_gemm_fp8.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p, i64, vp, u8p, i64, vp, ctypes.c_int,
+                                  vp, i64, vp, vp, i64, vp]
+        L.uh_layer_fwd_fp8.argtypes = [P(Jagged), Mask, P(LayerParams), P(Fp8Weights), vp, vp, P(LayerSaved), vp,
+                                       sz, vp]
+        for f in ("uh_ln_fwd_fp8", "uh_gated_norm_fwd_fp8", "uh_quant_weight_fp8", "uh_gemm_fp8",
+                  "uh_layer_fwd_fp8"):
+            getattr(L, f).restype = ctypes.c_int
         if L.uh_abi_version() != 1:
             raise RuntimeError("libuhstu ABI version mismatch")
         _lib = L
@@ -115,7 +133,8 @@ def exported_symbols() -> list:
     return ["uh_status_string", "uh_last_error", "uh_abi_version", "uh_mask_nnz", "uh_batch_nnz",
             "uh_attn_workspace_bytes", "uh_attn_fwd", "uh_attn_bwd", "uh_layer_workspace_bytes", "uh_layer_fwd",
             "uh_layer_bwd", "uh_jagged_gather", "uh_jagged_slice_latest", "uh_jagged_to_padded",
-            "uh_padded_to_jagged", "uh_partition_lpt"]
+            "uh_padded_to_jagged", "uh_partition_lpt", "uh_ln_fwd_fp8", "uh_gated_norm_fwd_fp8",
+            "uh_quant_weight_fp8", "uh_gemm_fp8", "uh_layer_fwd_fp8"]
 
 
 def _check(st: int):
@@ -391,3 +410,74 @@ def partition_lpt(lengths, world: int, m: Mask, d: int, num_heads: int):
                                   owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
                                   cost.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
     return owner, cost
+
+
+# ----------------------------------------------------------------------------- NEXT-2: FP8 projections
+# (include/uhstu_fp8.h).  Codes are torch.uint8 tensors (E4M3 bit patterns).
+def _u8(T, d, dev):
+    return torch.empty(T, d, dtype=torch.uint8, device=dev)
+
+
+def ln_fwd_fp8(x, w, b, eps=1e-6, q=None, scale=None, mean=None, rstd=None):
+    """codes(LN(x)), row scales (and LN statistics when mean / rstd are given)."""
+    T, d = x.shape
+    q = _u8(T, d, x.device) if q is None else q
+    scale = torch.empty(T, dtype=torch.float32, device=x.device) if scale is None else scale
+    _check(lib().uh_ln_fwd_fp8(T, d, _ptr(x), x.stride(0), _ptr(w), _ptr(b), eps, _ptr(q), q.stride(0),
+                               _ptr(scale), _ptr(mean), _ptr(rstd), _stream()))
+    return q, scale
+
+
+def gated_norm_fwd_fp8(A, U_, w, b, eps=1e-6, q=None, scale=None, mean=None, rstd=None):
+    """codes(LN(A) (.) U), row scales."""
+    T, d = A.shape
+    q = _u8(T, d, A.device) if q is None else q
+    scale = torch.empty(T, dtype=torch.float32, device=A.device) if scale is None else scale
+    _check(lib().uh_gated_norm_fwd_fp8(T, d, _ptr(A), A.stride(0), _ptr(U_), U_.stride(0), _ptr(w), _ptr(b), eps,
+                                       _ptr(q), q.stride(0), _ptr(scale), _ptr(mean), _ptr(rstd), _stream()))
+    return q, scale
+
+
+def quant_weight_fp8(W):
+    """W bf16 [K, N] -> (W^T codes [N, K], per-column scales [N])."""
+    K, N = W.shape
+    qt = _u8(N, K, W.device)
+    s = torch.empty(N, dtype=torch.float32, device=W.device)
+    _check(lib().uh_quant_weight_fp8(K, N, _ptr(W), W.stride(0), _ptr(qt), qt.stride(0), _ptr(s), _stream()))
+    return qt, s
+
+
+def gemm_fp8(qa, sa, qb, sb, epi: int = 0, bias=None, resid=None, out=None):
+    """out = diag(sa) (qa qb^T) diag(sb) (+ bias)(+ resid) (epi 0) or silu(...) (epi 1), bf16."""
+    M, K = qa.shape
+    N = qb.shape[0]
+    out = torch.empty(M, N, dtype=torch.bfloat16, device=qa.device) if out is None else out
+    _check(lib().uh_gemm_fp8(M, N, K, _ptr(qa), qa.stride(0), _ptr(sa), _ptr(qb), qb.stride(0), _ptr(sb), epi,
+                             _ptr(out), out.stride(0), _ptr(bias), _ptr(resid),
+                             0 if resid is None else resid.stride(0), _stream()))
+    return out
+
+
+def quant_layer_weights(prm: Params):
+    """The layer's uh_fp8_weights (run once per weight update); returns (struct, keep-alive tensors)."""
+    w1t, s1 = quant_weight_fp8(prm.w1)
+    w2t, s2 = quant_weight_fp8(prm.w2)
+    return Fp8Weights(_ptr(w1t), _ptr(s1), _ptr(w2t), _ptr(s2)), (w1t, s1, w2t, s2)
+
+
+def layer_fwd_fp8(jag, m, prm: Params, attn: Attn, x, qw, save: bool = False, out=None, ws=None,
+                  saved: Optional[Saved] = None):
+    """out = HSTU layer(x) with both projections in FP8; qw from quant_layer_weights."""
+    out = torch.empty_like(x) if out is None else out
+    if save and saved is None:
+        saved = alloc_saved(x)
+    if not save:
+        saved = None
+    p = prm.c(attn)
+    if ws is None:
+        ws = _ws(layer_workspace_bytes(jag, m, prm, attn, BF16, False), x.device)
+    sc = saved.c() if saved is not None else None
+    st, _keep = qw
+    _check(lib().uh_layer_fwd_fp8(ctypes.byref(jag.c), m, ctypes.byref(p), ctypes.byref(st), _ptr(x), _ptr(out),
+                                  ctypes.byref(sc) if sc is not None else None, _ptr(ws), ws.numel(), _stream()))
+    return out, saved

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     names = []
-    for h in ("uhstu.h", "uhstu_testing.h"):
+    for h in ("uhstu.h", "uhstu_testing.h", "uhstu_fp8.h"):
         txt = open(os.path.join(ROOT, "include", h)).read()
         names += re.findall(r"UH_API\s+[\w\s\*]+?\b(uh_\w+)\s*\(", txt)
     return sorted(set(names))
@@ -25,7 +25,7 @@ def declared_symbols():
 
 def test_library_exports_every_declared_symbol():
     syms = declared_symbols()
-    assert len(syms) >= 17
+    assert len(syms) >= 22
     out = subprocess.run(["nm", "-D", "--defined-only", U.LIB_PATH], capture_output=True, text=True).stdout
     exported = set(re.findall(r"\sT\s(uh_\w+)", out))
     missing = [s for s in syms if s not in exported]

@@ -25,8 +25,12 @@ RAGGED = [0, 1, 2, 17, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 # walks several tiles (both TMEM accumulators, barrier phase flips)
 @pytest.mark.parametrize("MNK", [(256, 512, 128), (296, 256, 192), (128, 2048, 512), (768, 512, 1024),
                                  (37965, 512, 128)])
-def test_gemm_bf16_majors(a_mn, b_mn, MNK):
+@pytest.mark.parametrize("pair", ["0", "2"])   # UH_GEMM_PAIR=2: CTA-pair (cta_group::2) tiles where eligible
+def test_gemm_bf16_majors(a_mn, b_mn, MNK, pair, monkeypatch):
+    monkeypatch.setenv("UH_GEMM_PAIR", pair)
     M, N, K = MNK
+    if a_mn and M % 8:
+        pytest.skip("MN-major A is stored [K][M]: its row stride M must be a multiple of 8")
     g = torch.Generator().manual_seed(0)
     A = torch.randn(M, K, generator=g).bfloat16()
     B = torch.randn(K, N, generator=g).bfloat16()
@@ -43,7 +47,9 @@ def test_gemm_bf16_majors(a_mn, b_mn, MNK):
 
 @pytest.mark.parametrize("b_mn", [True, False])
 @pytest.mark.parametrize("M", [200, 20000])
-def test_gemm_bf16_silu_and_residual_epilogues(b_mn, M):
+@pytest.mark.parametrize("pair", ["0", "2"])
+def test_gemm_bf16_silu_and_residual_epilogues(b_mn, M, pair, monkeypatch):
+    monkeypatch.setenv("UH_GEMM_PAIR", pair)
     N, K = 512, 256
     g = torch.Generator().manual_seed(1)
     A = torch.randn(M, K, generator=g).bfloat16()
