@@ -114,7 +114,7 @@ def test_greedy_fill_bound_and_maximality():
     user left out would have pushed s over it when its turn came."""
     rng = np.random.default_rng(0)
     P = L.LbslParams(R=1, T_warm=1, T_recal=1, gamma=1.7, ell_sl=512, b=32)
-        for t in range(50):
+    for t in range(50):
         B = _pareto_batches(rng, 1, 32)[0]
         ell_bar = float(rng.uniform(0.8, 3.0)) * 32 * 512.0 ** 1.7
         dec, new = L.rank_select(B, P, ell_bar, True, 4, 0, t)
