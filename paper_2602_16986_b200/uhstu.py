@@ -118,6 +118,14 @@ def lib():
         for f in ("uh_ln_fwd_fp8", "uh_gated_norm_fwd_fp8", "uh_quant_weight_fp8", "uh_gemm_fp8",
                   "uh_layer_fwd_fp8"):
             getattr(L, f).restype = ctypes.c_int
+        # NEXT-3: LBSL (include/uhstu_lbsl.h)
+        u64, f64, P32 = ctypes.c_uint64, ctypes.c_double, P(i32)
+        L.uh_lbsl_select.argtypes = [P32, i32, i32, f64, f64, i32, u64, i32, i64, P32, P32, P(f64)]
+        L.uh_lbsl_subset.argtypes = [i32, i32, u64, i32, i64, i32, P32]
+        L.uh_lbsl_rows.argtypes = [P32, i32, P32, P32, u64, i32, i64, P32, P32]
+        L.uh_gather_rows.argtypes = [vp, i64, vp, i64, i64, i32, vp, i64, vp]
+        for f in ("uh_lbsl_select", "uh_lbsl_subset", "uh_lbsl_rows", "uh_gather_rows"):
+            getattr(L, f).restype = ctypes.c_int
         if L.uh_abi_version() != 1:
             raise RuntimeError("libuhstu ABI version mismatch")
         _lib = L
@@ -134,7 +142,8 @@ def exported_symbols() -> list:
             "uh_attn_workspace_bytes", "uh_attn_fwd", "uh_attn_bwd", "uh_layer_workspace_bytes", "uh_layer_fwd",
             "uh_layer_bwd", "uh_jagged_gather", "uh_jagged_slice_latest", "uh_jagged_to_padded",
             "uh_padded_to_jagged", "uh_partition_lpt", "uh_ln_fwd_fp8", "uh_gated_norm_fwd_fp8",
-            "uh_quant_weight_fp8", "uh_gemm_fp8", "uh_layer_fwd_fp8"]
+            "uh_quant_weight_fp8", "uh_gemm_fp8", "uh_layer_fwd_fp8", "uh_lbsl_select", "uh_lbsl_subset",
+            "uh_lbsl_rows", "uh_gather_rows"]
 
 
 def _check(st: int):
@@ -481,3 +490,50 @@ def layer_fwd_fp8(jag, m, prm: Params, attn: Attn, x, qw, save: bool = False, ou
     _check(lib().uh_layer_fwd_fp8(ctypes.byref(jag.c), m, ctypes.byref(p), ctypes.byref(st), _ptr(x), _ptr(out),
                                   ctypes.byref(sc) if sc is not None else None, _ptr(ws), ws.numel(), _stream()))
     return out, saved
+
+
+# ----------------------------------------------------------------------------- NEXT-3: LBSL
+# (include/uhstu_lbsl.h; Alg. 1).  Host arrays are numpy; the gather is on device.
+def _i32p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def lbsl_select(lengths, ell_sl: int, gamma: float, ell_bar: float, steady: bool, seed: int, rank: int, step: int):
+    """Alg. 1 lines 4-20 for one rank: (decision[b], new_len[b], proxy load)."""
+    n = np.ascontiguousarray(np.asarray(lengths, np.int32))
+    dec = np.zeros(len(n), np.int32)
+    new = np.zeros(len(n), np.int32)
+    proxy = ctypes.c_double(0.0)
+    _check(lib().uh_lbsl_select(_i32p(n), len(n), int(ell_sl), float(gamma), float(ell_bar), int(bool(steady)),
+                                int(seed) & (2 ** 64 - 1), int(rank), int(step), _i32p(dec), _i32p(new),
+                                ctypes.byref(proxy)))
+    return dec, new, proxy.value
+
+
+def lbsl_subset(n: int, tau: int, seed: int, rank: int, step: int, u: int):
+    idx = np.zeros(max(tau, 0), np.int32)
+    _check(lib().uh_lbsl_subset(int(n), int(tau), int(seed) & (2 ** 64 - 1), int(rank), int(step), int(u),
+                                _i32p(idx)))
+    return idx
+
+
+def lbsl_rows(offsets, decision, new_len, seed: int, rank: int, step: int):
+    """Source row of every kept token and the new offsets (host int32)."""
+    off = np.ascontiguousarray(np.asarray(offsets, np.int32))
+    dec = np.ascontiguousarray(np.asarray(decision, np.int32))
+    nl = np.ascontiguousarray(np.asarray(new_len, np.int32))
+    rows = np.zeros(int(nl.sum()), np.int32)
+    new_off = np.zeros(len(off), np.int32)
+    _check(lib().uh_lbsl_rows(_i32p(off), len(off) - 1, _i32p(dec), _i32p(nl), int(seed) & (2 ** 64 - 1), int(rank),
+                              int(step), _i32p(rows), _i32p(new_off)))
+    return rows, new_off
+
+
+def gather_rows(rows_dev: torch.Tensor, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """y[i] = x[rows[i]] on the device (uh_gather_rows)."""
+    assert rows_dev.dtype == torch.int32 and rows_dev.is_cuda and x.is_cuda and x.dim() == 2
+    n = rows_dev.numel()
+    y = out if out is not None else torch.empty(n, x.shape[1], dtype=x.dtype, device=x.device)
+    _check(lib().uh_gather_rows(_ptr(rows_dev), n, _ptr(x), x.stride(0), x.shape[1], x.element_size(), _ptr(y),
+                                y.stride(0), _stream()))
+    return y

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     names = []
-    for h in ("uhstu.h", "uhstu_testing.h", "uhstu_fp8.h"):
+    for h in ("uhstu.h", "uhstu_testing.h", "uhstu_fp8.h", "uhstu_lbsl.h"):
         txt = open(os.path.join(ROOT, "include", h)).read()
         names += re.findall(r"UH_API\s+[\w\s\*]+?\b(uh_\w+)\s*\(", txt)
     return sorted(set(names))
