@@ -2,11 +2,14 @@
 regime of long histories) and the device gather of the kept rows (HBM roofline: 2 bytes
 moved per kept element byte, read + write)."""
 import json
+import os
+import sys
 import time
 
 import numpy as np
 import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_16986_b200 import lbsl as NL
 from paper_2602_16986_b200 import uhstu as U
 
