@@ -502,6 +502,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # stdout carries only the JSON line: native libraries (NCCL's version banner) write to
+    # fd 1 from C, so point fd 1 at stderr and keep a private handle for the line
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
@@ -515,7 +520,7 @@ def main():
             import torch.distributed as dist
             dist.destroy_process_group()
     if line is not None:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=out, flush=True)
 
 
 if __name__ == "__main__":
