@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -125,3 +126,18 @@ def test_layer_bwd_requires_saved_set():
     st = L.uh_layer_bwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(p), U.F32, ctypes.c_void_p(0x1000), None,
                         ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1000), ctypes.byref(g), 0, None, 0, None)
     assert L.uh_status_string(st).decode() == "UH_ERR_CACHE_MISMATCH"
+
+
+def test_bench_reference_arm_prints_one_json_line():
+    """bench.py's contract: stdout carries exactly one JSON line (the oracle arm runs on CPU)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "3"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout[-2000:]
+    import json
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["steps"] == 1 and d["warmup"] >= 3
+    assert d["value"] > 0 and d["unit"] == "tokens/s" and d["n_gpus"] == 1
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
