@@ -314,42 +314,43 @@ def run_ours(args, rank, world, local_rank):
                  "frac_of_measured_bf16_burst": attn_tflops / peaks["bf16_tflops"],
                  "frac_of_datasheet_2250": attn_tflops / 2250.0,
                  "flop_convention": "4*dh*H*nnz fwd + 10*dh*H*nnz bwd (unmasked pairs only)"},
-        "roofline": roofline_bwd(bwd_flop, bwd_ms, peaks, cfg.name),
+        "roofline": roofline_bwd(bwd_flop, bwd_ms, peaks, cfg.name, T, d),
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "clocks": clocks, "e2e": e2e,
     }
+    if world > 1:
+        line["nccl"] = {"nranks": world, "version": ".".join(map(str, torch.cuda.nccl.version())),
+                        "NCCL_ALGO": os.environ.get("NCCL_ALGO", "auto (NCCL's choice)"),
+                        "collective": "all_reduce(SUM) of the fp32 gradient bucket, once per step"}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
     return line
 
 
-def roofline_bwd(bwd_flop: float, bwd_ms: float, peaks: dict, workload: str):
+ROOFLINE_PROFILE = "r02_ncu_attn_bwd_cfg3.json"   # ncu --set full of one uh_attn_bwd call at cfg3
+
+
+def roofline_bwd(bwd_flop: float, bwd_ms: float, peaks: dict, workload: str, T: int, d: int):
     """The dominant step, attention backward (B4, one uh_attn_bwd call: the fused key-major
-    kernel attn_bwd_fused_sm100 plus the dQ finish kernel; UH_ATTN_BWD=split selects the
-    two-kernel path) against the measured bf16 burst peak (timed alone).  achieved = 10 d_h H nnz
-    algorithmic FLOPs per launch / the CUDA-event time of the call; traffic = DRAM read + write
-    bytes per launch of the call's kernels from the committed ncu --set full capture of the same
-    workload (profiles/r01_ncu_attn_fused_cfg3.json; split: profiles/r01_ncu_attn_cfg3.json)."""
+    kernel attn_bwd_fused_sm100 plus the dQ finish kernel) against the measured bf16 burst peak
+    (timed alone).  achieved = 10 d_h H nnz algorithmic FLOPs per launch / the CUDA-event time of
+    the call; traffic = DRAM read + write bytes per launch of the call's kernels from the committed
+    ncu --set full capture of the same workload (profiles/ROOFLINE_PROFILE)."""
     achieved = bwd_flop / (bwd_ms / 1e3) / 1e12
     traffic = None
-    split = os.environ.get("UH_ATTN_BWD") == "split"
-    name = "r01_ncu_attn_cfg3.json" if split else "r01_ncu_attn_fused_cfg3.json"
-    prof = os.path.join(ROOT, "profiles", name)
+    prof = os.path.join(ROOT, "profiles", ROOFLINE_PROFILE)
     if workload == "cfg3" and os.path.exists(prof):
         with open(prof) as f:
             pr = json.load(f)
-        keys = ("dq", "dkv") if split else ("fused", "dq_finish")
-        traffic = sum(pr[k]["dram_read_bytes"] + pr[k]["dram_write_bytes"] for k in keys)
-    kern = ("attn_bwd_dq_sm100 + attn_bwd_dkv_sm100" if split else
-            "attn_bwd_fused_sm100 + dq_finish_k (+ a cudaMemsetAsync of the fp32 dQ accumulator)")
-    return {"kernel": f"attention backward ({kern}, one uh_attn_bwd call)",
+        traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in pr["kernels"])
+    algo_bytes = 7 * T * d * 2   # read Q, K, V, dA; write dQ, dK, dV (bf16 [T, d] each)
+    return {"kernel": "attention backward (attn_bwd_fused_sm100 + dq_finish_k, one uh_attn_bwd call)",
             "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16_tflops"], "peak_source": peaks["source"] + " (burst: timed alone)",
-            "algorithmic_flop_per_launch": bwd_flop, "traffic": traffic,
-            "traffic_note": f"DRAM bytes per launch (ncu --set full, profiles/{name}; the memset's 0.54 GB write is "
-                            "not in it); algorithmic minimum ~1.6e9 (read Q, K, V, dA; write dQ, dK, dV) plus the "
-                            "fp32 dQ accumulator (fused: 0.54 GB zeroed by the memset, read once by the finish "
-                            "kernel; 61% of the dQ reduction sectors miss L2 at cfg3, the bulk of the excess)"}
+            "algorithmic_flop_per_launch": bwd_flop, "traffic": traffic, "algorithmic_bytes_per_launch": algo_bytes,
+            "traffic_note": f"DRAM bytes per launch (ncu --set full, profiles/{ROOFLINE_PROFILE}); the algorithmic "
+                            f"minimum is 7 T d 2 = {algo_bytes / 1e9:.2f} GB (read Q, K, V, dA; write dQ, dK, dV); the "
+                            "excess is the fp32 dQ accumulator (zeroed, reduced into in L2, read by the finish kernel)"}
 
 
 # ----------------------------------------------------------------------------- cfg5: inference
@@ -497,9 +498,22 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
-    if args.warmup < 3:
+    warmup_requested = args.warmup
+    if args.warmup < 3:   # the contract's minimum; the line reports the warm-up actually run
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # self-launch: one process per GPU through torch.distributed.run (same as the driver's torchrun)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     # stdout carries only the JSON line: native libraries (NCCL's version banner) write to
@@ -520,6 +534,8 @@ def main():
             import torch.distributed as dist
             dist.destroy_process_group()
     if line is not None:
+        if warmup_requested != args.warmup:
+            line["warmup_requested"] = warmup_requested
         print(json.dumps(line), file=out, flush=True)
 
 

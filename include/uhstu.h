@@ -128,8 +128,7 @@ UH_API int64_t uh_batch_nnz(const uh_jagged* jag, uh_mask m);
 
 /* Workspace bytes for uh_attn_fwd (backward=0) or uh_attn_bwd (backward=1).  The bf16
  * backward's workspace holds the tile schedule and an fp32 [T, H*head_dim] dQ accumulator
- * (4 bytes per token and dQ column; zeroed inside the call), so it is ~T*H*head_dim*4 bytes;
- * with UH_ATTN_BWD=split in the environment it holds the two tile schedules only. */
+ * (4 bytes per token and dQ column; zeroed inside the call), so it is ~T*H*head_dim*4 bytes. */
 UH_API uh_status uh_attn_workspace_bytes(const uh_jagged* jag, uh_mask m, const uh_attn_desc* desc,
                                   uh_dtype dtype, int backward, size_t* bytes);
 
@@ -175,11 +174,16 @@ typedef struct {
 /* Saved-activation set for the rematerialising backward (Listing 1
  * saves {x, u, attn}; this build saves {x (the caller's input), attn} plus the
  * LayerNorm statistics and rematerialises U with V,Q,K — DESIGN.md §5).
- * attn: [T,d] (dtype), ld = d.  Stats fp32 [T].  All caller-owned. */
+ * attn: [T,d] (dtype), ld = d.  Stats fp32 [T].  All caller-owned.
+ * fingerprint: written by uh_layer_fwd / uh_layer_fwd_fp8 (a hash of the host offsets,
+ * the mask, the attention descriptor's shape and scalars, eps and dtype); uh_layer_bwd
+ * returns UH_ERR_CACHE_MISMATCH when it differs from the backward call's (S:303
+ * "wrong cache variant"), e.g. a backward with another mask than its forward. */
 typedef struct {
     void* attn;
     float* ln1_mean; float* ln1_rstd;
     float* ln2_mean; float* ln2_rstd;
+    uint64_t fingerprint;
 } uh_layer_saved;
 
 /* Parameter gradients, fp32, same shapes as the parameters.  b1/b2/pos/time may
@@ -236,7 +240,8 @@ UH_API uh_status uh_padded_to_jagged(const uh_jagged* dst, const void* y, int64_
 
 /* ---------------------------------------------------------------------------
  * Token-balanced partitioner (host, deterministic).
- * cost(L) = 3*(2 L d 4d + 2 L d d) + 14 * head_dim * H * uh_mask_nnz(m, L);
+ * cost(L) = 4*(2 L d 4d) + 3*(2 L d d) + 14 * head_dim * H * uh_mask_nnz(m, L)
+ * (the layer step's flops on the sequence: f1, remat f1, dW1, dx^; f2, dY, dW2; attention);
  * LPT: sequences by (cost desc, id asc), each to the least-loaded rank (lowest
  * id on ties).  Outputs rank_of_seq[B] and rank_cost[world] (host).
  * The load notion follows LBSL's "sum n_u^gamma".

@@ -278,10 +278,12 @@ def layer_backward(dout, offsets, prm: LayerParams, H: int, spec: AttnSpec, cach
 # token-balanced partitioner (load notion of P:112)
 # ----------------------------------------------------------------------------
 def seq_cost(L: int, d: int, H: int, K1: int, K2: int) -> float:
-    """c(L) = 3*(2 L d 4d + 2 L d d) + 14 d_h H nnz(L): fwd+bwd+remat GEMM flops plus
-    attention fwd (4 d_h) + bwd (10 d_h) flops per allowed pair."""
+    """c(L) = 4 (2 L d 4d) + 3 (2 L d d) + 14 d_h H nnz(L): the flops one layer step spends on a
+    length-L sequence.  f1-shaped GEMMs: forward f1 (Eq. 2), the remat f1
+    (P:187), dW1 and dx^ (Listing 1); f2-shaped: forward f2 (Eq. 4), dY and dW2
+    (P:563-567); attention 4 d_h forward + 10 d_h backward flops per allowed pair-head."""
     dh = d // H
-    return 3.0 * (2.0 * L * d * 4 * d + 2.0 * L * d * d) + 14.0 * dh * H * mask_nnz(L, K1, K2)
+    return 4.0 * (2.0 * L * d * 4 * d) + 3.0 * (2.0 * L * d * d) + 14.0 * dh * H * mask_nnz(L, K1, K2)
 
 
 def partition_lpt(lengths, world: int, d: int, H: int, K1: int, K2: int):
@@ -308,8 +310,9 @@ def partition_lpt(lengths, world: int, d: int, H: int, K1: int, K2: int):
 # quantisation are computed with the preceding layer norms (Fig. fp8).
 # Readings R17-R20: E4M3FN codes, round-to-nearest-even with
 # saturation at 448; activation scale per row s_r = amax_r / 448 (1 for an
-# all-zero row), weight scale per output column; the code is taken in fp32
-# (the kernel's precision: t = fp32(fp32(v) * fp32(448 / amax)), R19).
+# all-zero row), weight scale per output column; the oracle quantises by the
+# plain definition in fp64 (R19: the kernel's fp32 decision may pick the
+# adjacent code where x / s is within fp32 noise of a midpoint).
 # ----------------------------------------------------------------------------
 E4M3_MAX = 448.0
 
@@ -328,17 +331,15 @@ def e4m3_round(v):
 
 
 def quant_rows_e4m3(x):
-    """Row-wise FP8 quantisation (R18, R19).  x [R, C] -> (q [R, C] float64
-    holding E4M3 values, s [R] float64 holding the fp32 scale), x ~= q * s[:, None]."""
-    x32 = np.asarray(x, np.float64).astype(np.float32)
-    amax = np.abs(x32).max(axis=1) if x32.shape[1] else np.zeros(x32.shape[0], np.float32)
-    pos = amax > 0
-    one = np.float32(1.0)
-    safe = np.where(pos, amax, one).astype(np.float32)
-    inv = np.where(pos, np.float32(E4M3_MAX) / safe, one).astype(np.float32)     # fp32 division
-    s = np.where(pos, safe / np.float32(E4M3_MAX), one).astype(np.float32)
-    t = (x32 * inv[:, None]).astype(np.float32)                                   # fp32 product
-    return e4m3_round(t.astype(np.float64)), s.astype(np.float64)
+    """Row-wise FP8 quantisation (R18): the plain definition in fp64,
+    s_r = amax_r / 448 (1 for an all-zero row) and q = RNE_e4m3(x / s_r).  x [R, C] ->
+    (q [R, C] float64 holding E4M3 values, s [R] float64), x ~= q * s[:, None].
+    (The kernel takes the same steps in fp32; its codes may differ from these only where
+    x / s sits within fp32 rounding of an E4M3 midpoint -- reading R19.)"""
+    x = np.asarray(x, np.float64)
+    amax = np.abs(x).max(axis=1) if x.shape[1] else np.zeros(x.shape[0])
+    s = np.where(amax > 0, amax / E4M3_MAX, 1.0)
+    return e4m3_round(x / s[:, None]), s
 
 
 def quant_weight_e4m3(w):

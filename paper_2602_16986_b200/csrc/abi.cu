@@ -116,12 +116,35 @@ uh_status check_layer(const uh_jagged* jag, uh_mask m, const uh_layer_params* p,
     UH_TRY(check_desc(&p->attn, dt));
     const int d = p->attn.num_heads * p->attn.head_dim;
     if (dt == UH_BF16 && d % 64) return fail(UH_ERR_SHAPE, "bf16 layer requires d % 64 == 0");
+    // the row kernels (norm.cu) hold a row in registers: 8 x 16-byte vectors per lane at most
+    if (d > (dt == UH_BF16 ? 2048 : 1024)) return fail(UH_ERR_UNSUPPORTED, "layer d above the norm kernels' limit");
     UH_TRY(check_ptr(p->ln1_w, "ln1_w")); UH_TRY(check_ptr(p->ln1_b, "ln1_b"));
     UH_TRY(check_ptr(p->ln2_w, "ln2_w")); UH_TRY(check_ptr(p->ln2_b, "ln2_b"));
     UH_TRY(check_ptr(p->w1, "w1")); UH_TRY(check_ptr(p->w2, "w2"));
     UH_TRY(check_ptr(p->b1, "b1", false)); UH_TRY(check_ptr(p->b2, "b2", false));
     if (!(p->eps > 0.f)) return fail(UH_ERR_DOMAIN, "eps must be > 0");
     return UH_OK;
+}
+
+// Fingerprint of what a saved set depends on (FNV-1a over the host offsets, the mask and
+// the attention descriptor's shape and scalars): uh_layer_fwd writes it, uh_layer_bwd
+// rejects a saved set whose fingerprint differs (UH_ERR_CACHE_MISMATCH).
+uint64_t saved_fingerprint(const uh_jagged* jag, uh_mask m, const uh_layer_params* p, uh_dtype dt) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* data, size_t n) {
+        const uint8_t* b = static_cast<const uint8_t*>(data);
+        for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+    };
+    mix(&jag->num_seqs, sizeof(jag->num_seqs));
+    mix(&jag->total_tokens, sizeof(jag->total_tokens));
+    mix(jag->host_offsets, sizeof(int32_t) * (size_t)(jag->num_seqs + 1));
+    mix(&m, sizeof(m));
+    const uh_attn_desc& a = p->attn;
+    const int32_t shape[6] = {a.num_heads, a.head_dim, a.pos_bias ? a.pos_bias_len : 0,
+                              a.time_bias ? a.time_bias_len : 0, (int32_t)dt, 0};
+    mix(shape, sizeof(shape));
+    mix(&a.alpha, sizeof(float)); mix(&a.norm_n, sizeof(float)); mix(&p->eps, sizeof(float));
+    return h | 1ull;   // never 0: a zeroed (never-written) saved set always mismatches
 }
 
 }  // namespace
@@ -300,6 +323,7 @@ uh_status uh_layer_fwd(const uh_jagged* jag, uh_mask m, const uh_layer_params* p
     g2.B = p->w2; g2.ldb = d; g2.b_mn = true;
     g2.epi = EPI_BF16; g2.out0 = out; g2.ld0 = d; g2.bias = p->b2; g2.resid = x; g2.ldr = d;
     UH_TRY(gemm_run(g2, dtype, st));
+    if (saved) saved->fingerprint = saved_fingerprint(jag, m, p, dtype);
     return UH_OK;
 }
 
@@ -310,6 +334,9 @@ uh_status uh_layer_bwd(const uh_jagged* jag, uh_mask m, const uh_layer_params* p
     if (!saved) return fail(UH_ERR_CACHE_MISMATCH, "backward needs the saved set of uh_layer_fwd");
     if (!saved->attn || !saved->ln1_mean || !saved->ln1_rstd || !saved->ln2_mean || !saved->ln2_rstd)
         return fail(UH_ERR_CACHE_MISMATCH, "saved set incomplete");
+    if (saved->fingerprint != saved_fingerprint(jag, m, p, dtype))
+        return fail(UH_ERR_CACHE_MISMATCH, "saved set was written by a forward with a different batch, mask or "
+                                           "attention descriptor");
     if (!grads) return fail(UH_ERR_NULL, "grads NULL");
     if (!grads->ln1_w || !grads->ln1_b || !grads->w1 || !grads->ln2_w || !grads->ln2_b || !grads->w2)
         return fail(UH_ERR_NULL, "required parameter gradient NULL");
@@ -413,7 +440,10 @@ uh_status uh_partition_lpt(const int32_t* lengths, int32_t B, int32_t world, uh_
     for (int i = 0; i < B; ++i) {
         if (lengths[i] < 0) return fail(UH_ERR_DOMAIN, "negative length");
         const double L = lengths[i];
-        cost[i] = 3.0 * (2.0 * L * d * 4 * d + 2.0 * L * d * d) + 14.0 * dh * num_heads * (double)uh_mask_nnz(m, lengths[i]);
+        // the step's flops on this sequence: four f1-shaped GEMMs (f1, remat f1, dW1, dx^), three
+        // f2-shaped (f2, dY, dW2), attention 4 d_h forward + 10 d_h backward per allowed pair-head
+        cost[i] = 4.0 * (2.0 * L * d * 4 * d) + 3.0 * (2.0 * L * d * d) +
+                  14.0 * dh * num_heads * (double)uh_mask_nnz(m, lengths[i]);
     }
     std::vector<int> order(B);
     std::iota(order.begin(), order.end(), 0);
@@ -435,13 +465,16 @@ uh_status uh_partition_lpt(const int32_t* lengths, int32_t B, int32_t world, uh_
 #include "../../include/uhstu_testing.h"
 extern "C" uh_status uh_test_gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
                                   int64_t ldb, int b_mn, int epi, void* out0, int64_t ld0, void* out1, int64_t ld1,
-                                  const float* bias, const void* resid, int64_t ldr, uh_dtype dtype, void* stream) {
-    if (M < 0 || N < 0 || K < 0 || epi < 0 || epi > 2) return fail(UH_ERR_DOMAIN, "bad gemm arguments");
+                                  const float* bias, const void* resid, int64_t ldr, uh_dtype dtype, int cta_pair,
+                                  void* stream) {
+    if (M < 0 || N < 0 || K < 0 || epi < 0 || epi > 2 || cta_pair < 0 || cta_pair > 2)
+        return fail(UH_ERR_DOMAIN, "bad gemm arguments");
     GemmDesc g;
     g.M = M; g.N = N; g.K = K;
     g.A = A; g.lda = lda; g.a_mn = a_mn != 0;
     g.B = B; g.ldb = ldb; g.b_mn = b_mn != 0;
     g.epi = epi; g.out0 = out0; g.ld0 = ld0; g.out1 = out1; g.ld1 = ld1; g.bias = bias; g.resid = resid; g.ldr = ldr;
+    g.pair = cta_pair;
     return gemm_run(g, dtype, (cudaStream_t)stream);
 }
 
@@ -572,5 +605,6 @@ extern "C" uh_status uh_layer_fwd_fp8(const uh_jagged* jag, uh_mask m, const uh_
     g2.A = codes; g2.lda = d; g2.B = qw->w2t; g2.ldb = d;
     g2.epi = EPI_BF16; g2.out0 = out; g2.ld0 = d; g2.bias = p->b2; g2.resid = x; g2.ldr = d;
     UH_TRY(gemm_fp8_run(g2, rscale, qw->s2, st));
+    if (saved) saved->fingerprint = saved_fingerprint(jag, m, p, dtype);
     return UH_OK;
 }

@@ -15,8 +15,7 @@ namespace uh {
 uh_status attn_fwd_simt_launch(const AttnArgs& a, cudaStream_t st);
 uh_status attn_bwd_simt_launch(const AttnArgs& a, cudaStream_t st);
 uh_status attn_fwd_sm100_launch(const AttnArgs& a, cudaStream_t st, int64_t T);
-uh_status attn_bwd_sm100_launch(const AttnArgs& a, const AttnArgs& akv, cudaStream_t st, int64_t T);
-bool attn_bwd_fused();   // one-kernel backward (dQ through an fp32 accumulator) unless UH_ATTN_BWD=split
+uh_status attn_bwd_sm100_launch(const AttnArgs& akv, cudaStream_t st, int64_t T);
 
 namespace {
 
@@ -30,20 +29,16 @@ __host__ __device__ inline int item_cost(int mode, int t, int L, int BMt, int BN
     return (query_end(k0, BMt, L, K1, K2) - k0 + BNt - 1) / BNt;
 }
 
-// gridDim.x schedules at once: block i builds mode mode0 + i into items[i] (the backward's
-// query-tile and key-tile schedules in one launch)
+// one block: the query-tile (forward) or key-tile (backward) schedule of the batch
 __global__ void __launch_bounds__(kSchedThreads) build_schedule_k(const int32_t* __restrict__ offsets, int B, int H,
-                                                                  int BMt, int BNt, int K1, int K2, int mode0,
-                                                                  WorkItem* __restrict__ items0,
-                                                                  WorkItem* __restrict__ items1, int* counter) {
+                                                                  int BMt, int BNt, int K1, int K2, int mode,
+                                                                  WorkItem* __restrict__ items, int* counter) {
     using Scan = cub::BlockScan<int, kSchedThreads>;
     __shared__ int hist[kCostBuckets];
     __shared__ typename Scan::TempStorage tmp;
     constexpr int PER = kCostBuckets / kSchedThreads;
-    const int mode = mode0 + (int)blockIdx.x;
-    WorkItem* __restrict__ items = blockIdx.x ? items1 : items0;
     for (int i = threadIdx.x; i < kCostBuckets; i += kSchedThreads) hist[i] = 0;
-    if (threadIdx.x == 0 && counter) counter[blockIdx.x] = 0;
+    if (threadIdx.x == 0 && counter) *counter = 0;
     __syncthreads();
     // one warp per sequence, lanes over its tiles (long sequences have hundreds of tiles);
     // under SLA nearly every tile has the same cost: aggregate equal buckets per warp first
@@ -110,7 +105,7 @@ int64_t count_items(const uh_jagged* jag, int BMt, int H) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t items_q = 0, items_k = 0, counters = 0, dq_acc = 0, total = 0;
+    size_t items_q = 0, counters = 0, dq_acc = 0, total = 0;
 };
 
 int tile_rows(uh_dtype dt) { return dt == UH_BF16 ? 128 : 64; }
@@ -121,9 +116,8 @@ WsLayout ws_layout(const uh_jagged* jag, const uh_attn_desc* desc, uh_dtype dt, 
     const int64_t n = count_items(jag, BMt, desc->num_heads);
     size_t off = 0;
     w.items_q = off; off += align256(n * sizeof(WorkItem));
-    if (backward) { w.items_k = off; off += align256(n * sizeof(WorkItem)); }
     w.counters = off; off += 256;
-    if (backward && dt == UH_BF16 && attn_bwd_fused()) {   // fp32 dQ accumulator [T, H dh]
+    if (backward && dt == UH_BF16) {   // fp32 dQ accumulator [T, H dh]
         w.dq_acc = off;
         off += align256((size_t)jag->total_tokens * desc->num_heads * desc->head_dim * sizeof(float));
     }
@@ -159,13 +153,12 @@ static AttnArgs base_args(const AttnCall& c, uh_dtype dt) {
     return a;
 }
 
-// mode0 into items0; with items1 also mode0 + 1 into items1 (same launch, counter[0..1])
-static uh_status schedule(const AttnCall& c, uh_dtype dt, int mode0, WorkItem* items0, WorkItem* items1, int* counter) {
+static uh_status schedule(const AttnCall& c, uh_dtype dt, int mode, WorkItem* items, int* counter) {
     const int BMt = tile_rows(dt);
     const int BNt = dt == UH_BF16 ? 128 : 32;
-    build_schedule_k<<<items1 ? 2 : 1, kSchedThreads, 0, c.st>>>(c.jag->offsets, c.jag->num_seqs, c.desc->num_heads,
-                                                                 BMt, BNt, c.mask.window, c.mask.n_global, mode0,
-                                                                 items0, items1, counter);
+    build_schedule_k<<<1, kSchedThreads, 0, c.st>>>(c.jag->offsets, c.jag->num_seqs, c.desc->num_heads,
+                                                                 BMt, BNt, c.mask.window, c.mask.n_global, mode,
+                                                                 items, counter);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;
@@ -179,7 +172,7 @@ uh_status attn_fwd_run(const AttnCall& c, uh_dtype dt) {
     a.counter = (int*)(ws + w.counters);
     a.n_items = (int)count_items(c.jag, tile_rows(dt), a.H);
     if (a.n_items == 0) return UH_OK;
-    UH_TRY(schedule(c, dt, SCHED_Q, (WorkItem*)a.items, nullptr, a.counter));
+    UH_TRY(schedule(c, dt, SCHED_Q, (WorkItem*)a.items, a.counter));
     if (dt == UH_F32) return attn_fwd_simt_launch(a, c.st);
     return attn_fwd_sm100_launch(a, c.st, c.jag->total_tokens);
 }
@@ -193,20 +186,14 @@ uh_status attn_bwd_run(const AttnCall& c, uh_dtype dt) {
     a.n_items = (int)count_items(c.jag, tile_rows(dt), a.H);
     if (a.n_items == 0) return UH_OK;
     if (dt == UH_F32) {
-        UH_TRY(schedule(c, dt, SCHED_Q, (WorkItem*)a.items, nullptr, nullptr));
+        UH_TRY(schedule(c, dt, SCHED_Q, (WorkItem*)a.items, nullptr));
         return attn_bwd_simt_launch(a, c.st);
     }
-    AttnArgs akv = a;
-    akv.items = (const WorkItem*)(ws + w.items_k);
-    akv.counter = a.counter + 1;
-    if (attn_bwd_fused()) {   // key-tile schedule only
-        akv.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
-        akv.ld_acc = (int64_t)a.H * a.dh;
-        UH_TRY(schedule(c, dt, SCHED_K, (WorkItem*)akv.items, nullptr, akv.counter));
-    } else {
-        UH_TRY(schedule(c, dt, SCHED_Q, (WorkItem*)a.items, (WorkItem*)akv.items, a.counter));
-    }
-    return attn_bwd_sm100_launch(a, akv, c.st, c.jag->total_tokens);
+    // bf16: the key-tile schedule (one key-major fused kernel) and the fp32 dQ accumulator
+    a.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
+    a.ld_acc = (int64_t)a.H * a.dh;
+    UH_TRY(schedule(c, dt, SCHED_K, (WorkItem*)a.items, a.counter));
+    return attn_bwd_sm100_launch(a, c.st, c.jag->total_tokens);
 }
 
 }  // namespace uh

@@ -32,7 +32,6 @@ namespace uh {
 namespace {
 
 constexpr int DH = 128;
-constexpr int NUM_THREADS = 384;   // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle (dkv: 2nd MMA), w4-11 epilogue
 
 __device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t row, int col, const float* v,
                                                 const void* gate, int64_t ldg, float scale) {
@@ -59,633 +58,6 @@ __device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t 
         o[ch] = make_uint4(pack_bf16(w[ch * 8 + 0], w[ch * 8 + 1]), pack_bf16(w[ch * 8 + 2], w[ch * 8 + 3]),
                            pack_bf16(w[ch * 8 + 4], w[ch * 8 + 5]), pack_bf16(w[ch * 8 + 6], w[ch * 8 + 7]));
 }
-
-// ============================================================================ dq kernel
-namespace dq {
-constexpr int BM = 128, BN = 64;
-constexpr int QT = BM * DH * 2;         // Q / dA tile bytes (2 x 16 KB swizzled blocks)
-constexpr int KT = BN * DH * 2;         // K / V tile bytes (2 x 8 KB blocks)
-constexpr int STAGES = 3;               // (K, V) ring
-constexpr int NS = 2;                   // S / dP buffers in TMEM
-constexpr int S_COL = 0, DP_COL = 128, DQ_COL = 256, Q_COL = 384, DA_COL = 448;
-constexpr int TSL = 8 * 32 * 32 * 4;   // d time_bias partials [8 warps][32 buckets][32 lanes]
-constexpr int SMEM = 2 * QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512 + TSL;
-
-struct __align__(8) Bars {
-    uint64_t qa_full, qa_empty;
-    uint64_t kv_full[STAGES], kv_empty[STAGES];
-    uint64_t s_full[NS], ds_full[NS];
-    uint64_t dq_full, dq_empty;
-    ItemRing ring;
-    uint32_t tmem;
-};
-
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-attn_bwd_dq_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sdA = smem + QT;
-    uint8_t* sKV = smem + 2 * QT;                     // [STAGES] x (K 16 KB | V 16 KB)
-    float* pos_s = reinterpret_cast<float*>(sKV + STAGES * 2 * KT);
-    float* ts_s = pos_s + kPosTab;
-    Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    TRACE_SETUP();
-
-    if (threadIdx.x == 0) {
-        mbar_init(&bars->qa_full, 1); mbar_init(&bars->qa_empty, 1);
-        for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
-        for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->ds_full[i], 8); }
-        mbar_init(&bars->dq_full, 1); mbar_init(&bars->dq_empty, 8);
-        ring_init(&bars->ring, 9);   // MMA warp + 8 epilogue warps
-        fence_barrier_init();
-    }
-    stage_rab(a, pos_s, ts_s);
-    float* tsl = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);   // [8 warps][32 buckets][32 lanes]
-    for (int i = threadIdx.x; i < TSL / 4; i += NUM_THREADS) tsl[i] = 0.f;
-    if (warp == 2) tmem_alloc<512>(&bars->tmem);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = bars->tmem;
-
-    if (warp == 0) {
-        // ============================================================ producer
-        if (lane == 0) {
-            int kc = 0, qi = 0;
-            for (;; ++qi) {
-                const int w = ring_claim_publish(&bars->ring, qi, a.counter, a.n_items);
-                if (w < 0) break;
-                const WorkItem it = a.items[w];
-                const int q0 = it.tile * BM, h = it.head & 0xFFFF;
-                const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
-                const int n = key_tiles_count(kt);
-                mbar_wait_sleep(&bars->qa_empty, (qi & 1) ^ 1);
-                mbar_arrive_expect_tx(&bars->qa_full, 2 * QT);
-                tma_load_2d(sQ, &tmQ, &bars->qa_full, h * DH, it.seq_start + q0);
-                tma_load_2d(sQ + QT / 2, &tmQ, &bars->qa_full, h * DH + 64, it.seq_start + q0);
-                tma_load_2d(sdA, &tmdA, &bars->qa_full, h * DH, it.seq_start + q0);
-                tma_load_2d(sdA + QT / 2, &tmdA, &bars->qa_full, h * DH + 64, it.seq_start + q0);
-                for (int j = 0; j < n; ++j) {
-                    const int row = it.seq_start + key_tile_at(kt, j) * BN;
-                    const int s = kc % STAGES;
-                    uint8_t* st = sKV + s * 2 * KT;
-                    mbar_wait_sleep(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
-                    tma_load_2d(st, &tmK, &bars->kv_full[s], h * DH, row);
-                    tma_load_2d(st + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
-                    tma_load_2d(st + KT, &tmV, &bars->kv_full[s], h * DH, row);
-                    tma_load_2d(st + KT + KT / 2, &tmV, &bars->kv_full[s], h * DH + 64, row);
-                    ++kc;
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ============================================================ MMA issuer
-        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [Q|dA](TMEM) x [K|V]^T
-        constexpr uint32_t idesc_q = make_idesc_bf16(BM, DH, false, true);    // dS (TMEM) x K (MN-major)
-        int kc = 0, sc = 0, qi = 0;
-        const uint32_t q_addr = smem_u32(sQ), da_addr = smem_u32(sdA);
-        for (;; ++qi) {
-            const int w = ring_take(&bars->ring, qi, lane);
-            if (w < 0) break;
-            const WorkItem it = a.items[w];
-            const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
-            const int n = key_tiles_count(kt);
-            mbar_wait(&bars->qa_full, qi & 1);
-            tc_fence_after();
-            if (elect_one()) {   // Q, dA: smem -> TMEM (ordered with the MMAs of the previous item)
-#pragma unroll
-                for (int kk = 0; kk < DH / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (QT / 2) + (kk & 3) * 32;
-                    tmem_cp_128x256b(tmem + Q_COL + kk * 8, make_sw128_desc(q_addr + off, 16, 1024));
-                    tmem_cp_128x256b(tmem + DA_COL + kk * 8, make_sw128_desc(da_addr + off, 16, 1024));
-                }
-                umma_commit(&bars->qa_empty);
-            }
-            __syncwarp();
-            // S(j) / dP(j) run one tile ahead of dQ(j - 1).  The next block's barrier is probed
-            // (test_wait) before the current block's MMAs are issued and waited on after them.
-            int s_st = kc % STAGES, s_ph = (kc / STAGES) & 1, s_sb = sc & 1;
-            int p_st = s_st, p_b = sc & 1, p_ph = (sc >> 1) & 1;
-            mbar_wait(&bars->kv_full[s_st], s_ph);
-            for (int j = 0; j <= n; ++j) {
-                if (j < n) {   // ---- S(j) = Q K_j^T, dP(j) = dA V_j^T
-                    tc_fence_after();
-                    // next block: dQ(j - 1) if j >= 1, else S(1) if n > 1, else dQ(0)
-                    const bool nxt_p = j >= 1 || n == 1;
-                    const int ns_st = s_st + 1 == STAGES ? 0 : s_st + 1, ns_ph = s_st + 1 == STAGES ? s_ph ^ 1 : s_ph;
-                    uint64_t* nb = nxt_p ? &bars->ds_full[p_b] : &bars->kv_full[ns_st];
-                    const uint32_t np = nxt_p ? p_ph : ns_ph;
-                    const bool rdy = mbar_test(smem_u32(nb), np);
-                    if (elect_one()) {
-                        const uint32_t k_addr = smem_u32(sKV + s_st * 2 * KT), v_addr = k_addr + KT;
-#pragma unroll
-                        for (int kk = 0; kk < DH / 16; ++kk) {
-                            const uint32_t ob = (kk >> 2) * (KT / 2) + (kk & 3) * 32;
-                            umma_ts(tmem + S_COL + s_sb * BN, tmem + Q_COL + kk * 8, make_sw128_desc(k_addr + ob, 16, 1024),
-                                    idesc_s, kk > 0 ? 1u : 0u);
-                            umma_ts(tmem + DP_COL + s_sb * BN, tmem + DA_COL + kk * 8,
-                                    make_sw128_desc(v_addr + ob, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-                        }
-                        umma_commit(&bars->s_full[s_sb]);
-                    }
-                    __syncwarp();
-                    s_st = ns_st; s_ph = ns_ph; s_sb ^= 1;
-                    ++kc; ++sc;
-                    if (!rdy) mbar_wait(nb, np);
-                }
-                if (j >= 1) {  // ---- dQ += dS(jj) K_jj  (dS over the consumed S columns)
-                    const int jj = j - 1;
-                    if (jj == 0) mbar_wait(&bars->dq_empty, (qi & 1) ^ 1);
-                    tc_fence_after();
-                    // next block: S(j + 1) if it exists, else dQ(j) if it exists, else none
-                    const bool nxt_s = j + 1 < n;
-                    const int np_b = p_b ^ 1, np_ph = p_b == 1 ? p_ph ^ 1 : p_ph;
-                    uint64_t* nb = nxt_s ? &bars->kv_full[s_st] : &bars->ds_full[j < n ? np_b : p_b];
-                    const uint32_t np = nxt_s ? s_ph : (j < n ? np_ph : p_ph);
-                    const bool rdy = mbar_test(smem_u32(nb), np);
-                    if (elect_one()) {
-                        const uint32_t k_addr = smem_u32(sKV + p_st * 2 * KT);
-#pragma unroll
-                        for (int kk = 0; kk < BN / 16; ++kk)
-                            umma_ts(tmem + DQ_COL, tmem + S_COL + p_b * BN + (kk >> 1) * 32 + (kk & 1) * 8,
-                                    make_sw128_desc(k_addr + kk * 2048, KT / 2, 1024), idesc_q,
-                                    (jj > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit(&bars->kv_empty[p_st]);
-                        if (jj == n - 1) umma_commit(&bars->dq_full);
-                    }
-                    __syncwarp();
-                    p_st = p_st + 1 == STAGES ? 0 : p_st + 1;
-                    p_b = np_b; p_ph = np_ph;
-                    if (!rdy) mbar_wait(nb, np);
-                }
-            }
-        }
-    } else if (warp >= 4) {
-        // ============================================================ epilogue
-        const int wg = (warp - 4) >> 2, wq = warp & 3;
-        const int r = wq * 32 + lane;
-        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const int et = threadIdx.x - 128;  // 0..255 among epilogue threads
-        const float ha = 0.5f * a.alpha;
-        const float rscale = 0.5f * a.inv_n;   // ds = rscale * ds'  (ds' is what the kernel carries)
-        // d rab partials live in registers / per-warp shared rows and reach global memory once
-        // per CTA (same-address global atomics from every row would serialise)
-        float far_acc = 0.f;       // d pos_bias[P-1] (total minus the near diagonals), in ds' units
-        float dpr[kMaxNearT];      // near diagonals lane + 32 t (tile offsets are multiples of 32)
-#pragma unroll
-        for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
-        int sc = 0, qi = 0;
-        for (;; ++qi) {
-            const int w = ring_take(&bars->ring, qi, lane);
-            if (w < 0) break;
-            const WorkItem it = a.items[w];
-            const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
-            const int q0 = it.tile * BM;
-            const KeyTiles kt = key_tiles(q0, BM, L, a.K1, a.K2, BN);
-            const int n = key_tiles_count(kt);
-            const int qp = q0 + r;
-            const bool qok = qp < L;
-            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
-            const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
-            // d rab partials of one 32-column chunk; runs after ds_full (off the S -> dS -> next-S
-            // chain, overlapping the tensor pipe).  d time_bias goes to this lane's own column of
-            // a shared [bucket][lane] table (conflict-free, no atomics, no local memory).
-            float* const tsl_l = tsl + (warp - 4) * 1024 + lane;
-            auto rab_grads = [&](const Chunk& ch, const uint32_t* d2, int kb) {
-                const float tsum = sum_packed16(d2);   // rows beyond L carry zeros
-                if (a.dts) {
-                    if (!(ch.flags & FLAG_T2)) {
-                        float so = 0.f;                // columns [0, n) are in bucket b_other (FLAG_T1)
-                        if ((ch.flags & FLAG_T1) && ch.n > 0) {
-                            uint32_t m2[16];
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                m2[i] = d2[i] & (2 * i + 1 < ch.n ? 0xFFFFFFFFu : (2 * i < ch.n ? 0x0000FFFFu : 0u));
-                            so = sum_packed16(m2);
-                            if (qok) tsl_l[ch.b_other * 32] += so;
-                        }
-                        if (qok) tsl_l[ch.b_base * 32] += tsum - so;
-                    } else {                           // next to the diagonal: per-element buckets,
-                        int bk[32];                    // monotone along the row (runs flushed on change)
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) bk[c] = bucket32(tq - __shfl_sync(0xffffffffu, ch.tcol, c), cx.NB);
-                        if (qok) {
-                            int cur = bk[0];
-                            float acc = 0.f;
-#pragma unroll
-                            for (int c = 0; c < 32; ++c) {
-                                const float2 u = unpack_bf16x2(d2[c >> 1]);
-                                if (bk[c] != cur) { tsl_l[cur * 32] += acc; cur = bk[c]; acc = 0.f; }
-                                acc += (c & 1) ? u.y : u.x;
-                            }
-                            tsl_l[cur * 32] += acc;
-                        }
-                    }
-                }
-                far_acc += tsum;
-                // near diagonals (delta <= P-2): delta = C + lane - c with C a multiple of 32;
-                // a skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
-                if (a.dpos) {
-                    const int C = q0 - kb + 32 * wq;
-                    if (C >= -31 && C <= a.P + 29) {   // warp-uniform
-                        float lo_s = 0.f, hi_s = 0.f;
-#pragma unroll
-                        for (int c = 0; c < 32; ++c) {
-                            const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (lane + c) & 31));
-                            const float xv = (c & 1) ? u.y : u.x;
-                            if (lane + c < 32) lo_s += xv; else hi_s += xv;
-                        }
-                        const int dlo = C + lane, dhi = C + lane - 32;
-                        const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
-                        const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
-#pragma unroll
-                        for (int t = 0; t < kMaxNearT; ++t) {
-                            dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
-                            dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
-                        }
-                        far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
-                    }
-                }
-            };
-            // every tile is split between the warpgroups by column (warpgroup wg: keys
-            // [32 wg, 32 wg + 32)), so tile j+1's epilogue overlaps tile j's dS -> dQ -> S(j+2) chain
-            for (int j = 0; j < n; ++j, ++sc) {
-                const int sb = sc % NS;
-                const int kb = key_tile_at(kt, j) * BN + 32 * wg;
-                const int32_t tcw = col_time(cx, kb, lane);
-                mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
-                tc_fence_after();
-                if ((warp & 3) == 0 && lane == 0) TRACE((4 + wg * 2) * 1024 + (sc & 1023));
-                const Chunk ch = q_chunk(cx, qp, qok, tq, kb, tcw);
-                uint32_t d2[16];
-                {
-                    float sv[32], dp[32];
-                    tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * wg, sv);
-                    tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * wg, dp);
-                    tmem_ld_wait();
-                    // ds' = dP (1 + t)(1 + h (1 - t)), h = (alpha S + rab)/2, t = tanh(h)  (== 2 N ds), bf16x2
-                    float hx[32];
-                    q_h<false>(cx, ch, tq, sv, hx, nullptr);
-                    if (ch.flags & FLAG_M) apply_vis(dp, q_vis_bits(cx, qp, qok, kb));   // dP = 0 -> dS = 0
-                    const uint64_t one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {   // fp32 pairs: (1 + t)(1 + h (1 - t)) dP, one bf16 pack
-                        const uint64_t H = f2_pack(hx[2 * i], hx[2 * i + 1]);
-                        const uint64_t T = f2_pack(tanh_approx(hx[2 * i]), tanh_approx(hx[2 * i + 1]));
-                        const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
-                        const float2 v = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * i], dp[2 * i + 1]), fadd2(T, one2)), W));
-                        d2[i] = pack_bf16(v.x, v.y);
-                    }
-                }
-                if (!qok) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) d2[i] = 0u;
-                }
-                // dS -> TMEM over this chunk's consumed S columns (A operand of dQ += dS K)
-                tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, d2);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->ds_full[sb]);
-                if ((warp & 3) == 0 && lane == 0) TRACE((5 + wg * 2) * 1024 + (sc & 1023));
-                if (a.dpos || a.dts) rab_grads(ch, d2, kb);
-            }
-            // ---- dQ epilogue: dQ = alpha/(2N) * (dS' K)
-            mbar_wait_sleep(&bars->dq_full, qi & 1);
-            tc_fence_after();
-            float v[64];
-            tmem_ld32(tmem + lane_base + DQ_COL + wg * 64, v);
-            tmem_ld32(tmem + lane_base + DQ_COL + wg * 64 + 32, v + 32);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->dq_empty);
-            if (qok) store_out_row64(a.dq, a.ld_grad, o + qp, h * DH + wg * 64, v, a.gq, a.ld_gate, ha * a.inv_n);
-        }
-        // ---- CTA-level reduction of the d rab partials, then one global atomic per entry
-        if (a.dpos || a.dts) {
-            float* redp = reinterpret_cast<float*>(sQ);          // Q/dA staging is no longer in use:
-            const int ew = et >> 5;                              // [kMaxNearT*32][8 warps] + far[8]
-            if (a.dpos) {
-#pragma unroll
-                for (int t = 0; t < kMaxNearT; ++t) redp[(t * 32 + lane) * 8 + ew] = dpr[t];
-            }
-            float f = far_acc;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
-            if (lane == 0) redp[kMaxNearT * 32 * 8 + ew] = f;
-            named_bar_sync(2, 256);
-            if (a.dts) {                       // bucket et >> 3, warp et & 7: 32 lanes, then 8 warps
-                const int b = et >> 3, w8 = et & 7;
-                float sum = 0.f;
-#pragma unroll 8
-                for (int l = 0; l < 32; ++l) sum += tsl[(w8 * 32 + b) * 32 + l];
-                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-                sum += __shfl_xor_sync(0xffffffffu, sum, 4);
-                if (w8 == 0 && b < a.NB && sum != 0.f) atomicAdd(a.dts + b, sum * rscale);
-            }
-            if (a.dpos) {
-                if (et < a.P - 1) {
-                    float sum = 0.f;
-#pragma unroll
-                    for (int w8 = 0; w8 < 8; ++w8) sum += redp[et * 8 + w8];
-                    if (sum != 0.f) atomicAdd(a.dpos + et, sum * rscale);
-                }
-                if (et == 0) {
-                    float sum = 0.f;
-#pragma unroll
-                    for (int w8 = 0; w8 < 8; ++w8) sum += redp[kMaxNearT * 32 * 8 + w8];
-                    if (sum != 0.f) atomicAdd(a.dpos + a.P - 1, sum * rscale);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (warp == 2) tmem_dealloc<512>(tmem);
-}
-}  // namespace dq
-
-// ============================================================================ dkv kernel
-#if UH_TRACE == 2
-#define TRACE_DKV(x) TRACE(x)
-#else
-#define TRACE_DKV(x) do { } while (0)
-#endif
-namespace dkv {
-constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per step
-constexpr int KT = BM * DH * 2;           // K / V tile (32 KB: 2 x 16 KB blocks of [128 rows x 128 B])
-constexpr int QT = BN * DH * 2;           // Q / dA tile (16 KB: 2 x 8 KB blocks of [64 rows x 128 B])
-constexpr int KV_BUFS = 2;                // (K, V) double buffer: the next item's load overlaps this item
-constexpr int STAGES = 3;                 // (Q, dA) ring
-constexpr int NS = 2;                     // S^T / dP^T buffers
-constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-constexpr int SMEM_DATA = KV_BUFS * 2 * KT + STAGES * 2 * QT + kPosTab * 4 + 256 + 512;
-constexpr int SMEM = 232448;              // the opt-in maximum: data plus as much alignment slack as remains
-static_assert(SMEM_DATA <= SMEM, "dkv shared memory");
-
-struct __align__(8) Bars {
-    uint64_t kv_full[KV_BUFS], kv_empty[KV_BUFS];
-    uint64_t qa_full[STAGES], qa_empty[STAGES];
-    uint64_t s_full[NS], p_full[NS];
-    uint64_t issued[NS];          // dV/dK of the step in buffer b issued (orders the next S^T into b)
-    uint64_t acc_full, acc_empty;
-    ItemRing ring;
-    uint32_t tmem;
-};
-
-__device__ __forceinline__ int n_qtiles(int k0, int L, int K1, int K2) {
-    const int qe = query_end(k0, BM, L, K1, K2);
-    return (qe + BN - 1) / BN - k0 / BN;
-}
-
-// Per 128-key tile (K, V resident in shared memory for the whole item), over the 64-query
-// tiles that see it: S^T = K Q^T and dP^T = V dA^T (SS, N = 64) into TMEM; the epilogue
-// (warpgroup wg: queries [32 wg, 32 wg + 32)) writes P^T and dS^T (bf16) over the consumed
-// columns; dV += P^T dA and dK += dS^T Q read them as TMEM A operands.  64-query steps keep
-// the MMA issuer's per-step overhead (barrier waits, commits) well under the tensor time.
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-attn_bwd_dkv_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA, AttnArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    if (threadIdx.x == 0 && (smem - smem_raw) + SMEM_DATA > SMEM) __trap();   // alignment slack exhausted
-    uint8_t* sKV = smem;                          // [KV_BUFS] x (K 32 KB | V 32 KB)
-    uint8_t* sQA = smem + KV_BUFS * 2 * KT;       // [STAGES] x (Q 16 KB | dA 16 KB)
-    float* pos_s = reinterpret_cast<float*>(sQA + STAGES * 2 * QT);
-    float* ts_s = pos_s + kPosTab;
-    Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    TRACE_SETUP();
-
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < KV_BUFS; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
-        for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->qa_full[i], 1); mbar_init(&bars->qa_empty[i], 1); }
-        for (int i = 0; i < NS; ++i) {
-            mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 8); mbar_init(&bars->issued[i], 1);
-        }
-        mbar_init(&bars->acc_full, 1); mbar_init(&bars->acc_empty, 8);
-        ring_init(&bars->ring, 10);  // MMA warps 1, 3 + 8 epilogue warps
-        fence_barrier_init();
-    }
-    stage_rab(a, pos_s, ts_s);
-    if (warp == 2) tmem_alloc<512>(&bars->tmem);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = bars->tmem;
-
-    if (warp == 0) {
-        // ============================================================ producer
-        if (lane == 0) {
-            int qc = 0, ki = 0;
-            for (;; ++ki) {
-                const int w = ring_claim_publish(&bars->ring, ki, a.counter, a.n_items);
-                if (w < 0) break;
-                const WorkItem it = a.items[w];
-                const int k0 = it.tile * BM, h = it.head & 0xFFFF;
-                const int n = n_qtiles(k0, it.seq_len, a.K1, a.K2);
-                const int kb = ki & 1;
-                uint8_t* sK = sKV + kb * 2 * KT;
-                mbar_wait_sleep(&bars->kv_empty[kb], ((ki >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bars->kv_full[kb], 2 * KT);
-                tma_load_2d(sK, &tmK, &bars->kv_full[kb], h * DH, it.seq_start + k0);
-                tma_load_2d(sK + KT / 2, &tmK, &bars->kv_full[kb], h * DH + 64, it.seq_start + k0);
-                tma_load_2d(sK + KT, &tmV, &bars->kv_full[kb], h * DH, it.seq_start + k0);
-                tma_load_2d(sK + KT + KT / 2, &tmV, &bars->kv_full[kb], h * DH + 64, it.seq_start + k0);
-                for (int i = 0; i < n; ++i) {
-                    const int row = it.seq_start + (k0 / BN + i) * BN;
-                    const int s = qc % STAGES;
-                    uint8_t* st = sQA + s * 2 * QT;
-                    mbar_wait_sleep(&bars->qa_empty[s], ((qc / STAGES) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&bars->qa_full[s], 2 * QT);
-                    tma_load_2d(st, &tmQ, &bars->qa_full[s], h * DH, row);
-                    tma_load_2d(st + QT / 2, &tmQ, &bars->qa_full[s], h * DH + 64, row);
-                    tma_load_2d(st + QT, &tmdA, &bars->qa_full[s], h * DH, row);
-                    tma_load_2d(st + QT + QT / 2, &tmdA, &bars->qa_full[s], h * DH + 64, row);
-                    ++qc;
-                }
-            }
-        }
-    } else if (warp == 1 || warp == 3) {
-        // ============================================================ MMA issuers
-        // Two warps feed the one tensor pipe: warp 1 issues S^T / dP^T, warp 3 issues dV / dK, so
-        // one warp's barrier wait (~130 cycles even when complete) overlaps the other's issue and
-        // the 4-5 deep MMA queue does not drain.  S^T(i + 2) reuses the TMEM buffer that
-        // dV/dK(i) reads: warp 1 waits for "issued" (fence::before/after_thread_sync around it
-        // order the two warps' tcgen05.mma in the pipe).  Each warp runs convergently
-        // (descriptors in uniform registers); one elected lane issues each block.
-        constexpr uint32_t idesc_s = make_idesc_bf16(BM, BN, false, false);   // [K|V] x [Q|dA]^T (both K-major)
-        constexpr uint32_t idesc_a = make_idesc_bf16(BM, DH, false, true);    // [P^T|dS^T](TMEM) x [dA|Q] (MN-major)
-        int ki = 0, sc = 0;
-        if (warp == 1) {
-            const uint64_t kv_k = make_sw128_desc(smem_u32(sKV), 16, 1024);      // K / V K-major (A)
-            const uint64_t q_k = make_sw128_desc(smem_u32(sQA), 16, 1024);       // Q / dA K-major (B)
-            int st_s = 0, ph_s = 0;
-            for (;; ++ki) {
-                const int w = ring_take(&bars->ring, ki, lane);
-                if (w < 0) break;
-                const WorkItem it = a.items[w];
-                const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
-                const int kb = ki & 1;
-                const uint64_t dk = kv_k + ((uint32_t)(kb * 2 * KT) >> 4), dv = dk + (KT >> 4);
-                mbar_wait(&bars->kv_full[kb], (ki >> 1) & 1);
-                mbar_wait(&bars->qa_full[st_s], ph_s);
-                mbar_wait(&bars->issued[sc & 1], ((sc >> 1) - 1) & 1);   // (first steps: parity 1 of a fresh barrier passes)
-                for (int i = 0; i < n; ++i, ++sc) {   // ---- S^T(i) = K Q_i^T, dP^T(i) = V dA_i^T
-                    const int sb = sc & 1;
-                    tc_fence_after();
-                    // probe step i+1's barriers now, wait on them after this step's MMAs are issued
-                    const int nst = st_s + 1 == STAGES ? 0 : st_s + 1, nph = st_s + 1 == STAGES ? ph_s ^ 1 : ph_s;
-                    const uint32_t qa_a = smem_u32(&bars->qa_full[nst]), is_a = smem_u32(&bars->issued[sb ^ 1]);
-                    const uint32_t is_p = (((sc + 1) >> 1) - 1) & 1;
-                    const bool r1 = mbar_test(qa_a, nph), r2 = mbar_test(is_a, is_p);
-                    const uint64_t dq = q_k + ((uint32_t)(st_s * 2 * QT) >> 4), dda = dq + (QT >> 4);
-                    const uint32_t d_s = tmem + S_COL + sb * BN, d_p = tmem + DP_COL + sb * BN;
-                    if (elect_one()) {
-#pragma unroll
-                        for (int kk = 0; kk < DH / 16; ++kk) {
-                            const uint32_t oa = ((kk >> 2) * (KT / 2) + (kk & 3) * 32) >> 4;
-                            const uint32_t ob = ((kk >> 2) * (QT / 2) + (kk & 3) * 32) >> 4;
-                            umma_ss(d_s, dk + oa, dq + ob, idesc_s, kk > 0 ? 1u : 0u);
-                            umma_ss(d_p, dv + oa, dda + ob, idesc_s, kk > 0 ? 1u : 0u);
-                        }
-                        umma_commit(&bars->s_full[sb]);
-                        if (i == n - 1) umma_commit(&bars->kv_empty[kb]);   // K, V read by the last S^T / dP^T
-                    }
-                    __syncwarp();
-                    st_s = nst; ph_s = nph;
-                    if (i + 1 < n) {
-                        if (!r1) mbar_wait_addr(qa_a, nph);
-                        if (!r2) mbar_wait_addr(is_a, is_p);
-                    }
-                }
-            }
-        } else {
-            const uint64_t q_mn = make_sw128_desc(smem_u32(sQA), QT / 2, 1024);  // Q / dA MN-major (B)
-            int st_a = 0;
-            for (;; ++ki) {
-                const int w = ring_take(&bars->ring, ki, lane);
-                if (w < 0) break;
-                const WorkItem it = a.items[w];
-                const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
-                mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
-                mbar_wait(&bars->p_full[sc & 1], (sc >> 1) & 1);
-                for (int i = 0; i < n; ++i, ++sc) {   // ---- dV += P^T dA, dK += dS^T Q
-                    const int pb = sc & 1;
-                    tc_fence_after();
-                    const uint32_t pf_a = smem_u32(&bars->p_full[pb ^ 1]), pf_p = ((sc + 1) >> 1) & 1;
-                    const bool r = mbar_test(pf_a, pf_p);   // step i+1's P^T / dS^T
-                    const uint64_t dq = q_mn + ((uint32_t)(st_a * 2 * QT) >> 4), dda = dq + (QT >> 4);
-                    const uint32_t a_p = tmem + S_COL + pb * BN, a_d = tmem + DP_COL + pb * BN;
-                    if (elect_one()) {
-#pragma unroll
-                        for (int kk = 0; kk < BN / 16; ++kk) {
-                            // queries [16 kk, 16 kk + 16): packed by warpgroup kk / 2 at column 32 (kk / 2) + 8 (kk % 2)
-                            const uint32_t ca = (kk >> 1) * 32 + (kk & 1) * 8;
-                            const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                            umma_ts(tmem + DV_COL, a_p + ca, dda + kk * (2048 >> 4), idesc_a, acc);
-                            umma_ts(tmem + DK_COL, a_d + ca, dq + kk * (2048 >> 4), idesc_a, acc);
-                        }
-                        umma_commit(&bars->qa_empty[st_a]);
-                        if (i == n - 1) umma_commit(&bars->acc_full);
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&bars->issued[pb]);
-                    if (++st_a == STAGES) st_a = 0;
-                    if (i + 1 < n && !r) mbar_wait_addr(pf_a, pf_p);
-                }
-            }
-        }
-    } else if (warp >= 4) {
-        // ============================================================ epilogue
-        const int wg = (warp - 4) >> 2, wq = warp & 3;
-        const int r = wq * 32 + lane;
-        const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
-        const float ha = 0.5f * a.alpha;
-        int sc = 0, ki = 0;
-        for (;; ++ki) {
-            const int w = ring_take(&bars->ring, ki, lane);
-            if (w < 0) break;
-            const WorkItem it = a.items[w];
-            const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
-            const int k0 = it.tile * BM;
-            const int n = n_qtiles(k0, L, a.K1, a.K2);
-            const int kp = k0 + r;
-            const bool kok = kp < L;
-            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
-            const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
-            for (int i = 0; i < n; ++i, ++sc) {
-                const int sb = sc % NS;
-                const int qb = (k0 / BN + i) * BN + 32 * wg;   // this warpgroup's 32 queries
-                const int32_t tcur = col_time(cx, qb, lane);
-                const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
-                mbar_wait_sleep(&bars->s_full[sb], (sc / NS) & 1);
-                tc_fence_after();
-#if UH_EXP == 1
-                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
-                continue;
-#endif
-                float sv[32], dp[32];
-                tmem_ld32(tmem + lane_base + S_COL + sb * BN + 32 * wg, sv);
-                tmem_ld32(tmem + lane_base + DP_COL + sb * BN + 32 * wg, dp);
-                tmem_ld_wait();
-                // p' = silu(2h) = h (1 + t);  ds' = dP (1 + t)(1 + h (1 - t));  t = tanh(h); bf16x2
-                float hx[32];
-                k_h(cx, ch, tk, sv, hx);
-                if (ch.flags & FLAG_M) {          // h = 0 and dP = 0 -> P = dS = 0
-                    const uint32_t m = k_vis_bits(cx, kp, kok, qb);
-                    apply_vis(hx, m);
-                    apply_vis(dp, m);
-                }
-                uint32_t p2[16], d2[16];
-                const uint64_t one2 = f2_pack(1.f, 1.f), neg2 = f2_pack(-1.f, -1.f);
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {   // fp32 pairs: P = h (1 + t), dS = dP (1 + t)(1 + h (1 - t))
-                    const uint64_t H = f2_pack(hx[2 * c], hx[2 * c + 1]);
-                    const uint64_t T = f2_pack(tanh_approx(hx[2 * c]), tanh_approx(hx[2 * c + 1]));
-                    const uint64_t A1 = fadd2(T, one2);
-                    const float2 pv = f2_unpack(fmul2(H, A1));
-                    p2[c] = pack_bf16(pv.x, pv.y);
-                    const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
-                    const float2 dv = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * c], dp[2 * c + 1]), A1), W));
-                    d2[c] = pack_bf16(dv.x, dv.y);
-                }
-                // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
-                tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);
-                tmem_st16(tmem + lane_base + DP_COL + sb * BN + 32 * wg, d2);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->p_full[sb]);
-                if (lane == 0 && (warp & 3) == 0) TRACE_DKV((6 + wg) * 1024 + (sc & 1023));
-            }
-            mbar_wait_sleep(&bars->acc_full, ki & 1);
-            tc_fence_after();
-            float dv[64], dk[64];
-            tmem_ld32(tmem + lane_base + DV_COL + wg * 64, dv);
-            tmem_ld32(tmem + lane_base + DV_COL + wg * 64 + 32, dv + 32);
-            tmem_ld32(tmem + lane_base + DK_COL + wg * 64, dk);
-            tmem_ld32(tmem + lane_base + DK_COL + wg * 64 + 32, dk + 32);
-            tmem_ld_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->acc_empty);
-            if (kok) {
-                store_out_row64(a.dv, a.ld_grad, o + kp, h * DH + wg * 64, dv, a.gv, a.ld_gate, a.inv_n);
-                store_out_row64(a.dk, a.ld_grad, o + kp, h * DH + wg * 64, dk, a.gk, a.ld_gate, ha * a.inv_n);
-            }
-        }
-    }
-    __syncthreads();
-    if (warp == 2) tmem_dealloc<512>(tmem);
-}
-}  // namespace dkv
 
 // ============================================================================ fused kernel
 // One pass per 128-key tile computes dV, dK and the dQ partials of every visible 64-query
@@ -1182,55 +554,26 @@ __global__ void __launch_bounds__(256) dq_finish_k(int64_t T, int width, const f
 
 }  // namespace
 
-static bool bwd_split() {   // UH_ATTN_BWD=split selects the two-kernel backward (A/B measurements)
-    static const int v = [] { const char* e = getenv("UH_ATTN_BWD"); return e && !strcmp(e, "split") ? 1 : 0; }();
-    return v != 0;
-}
-
-bool attn_bwd_fused() { return !bwd_split(); }
-
-uh_status attn_bwd_sm100_launch(const AttnArgs& aq, const AttnArgs& akv, cudaStream_t st, int64_t T) {
-    if (aq.dh != DH) return fail(UH_ERR_UNSUPPORTED, "bf16 attention requires head_dim == 128");
+uh_status attn_bwd_sm100_launch(const AttnArgs& akv, cudaStream_t st, int64_t T) {
+    if (akv.dh != DH) return fail(UH_ERR_UNSUPPORTED, "bf16 attention requires head_dim == 128");
     if (akv.n_items == 0) return UH_OK;
-    const uint64_t width = (uint64_t)aq.H * DH;
+    const uint64_t width = (uint64_t)akv.H * DH;
     const int sms = num_sms();
-    if (!bwd_split()) {
-        CUtensorMap q64, dA64, k128, v128, dqm;
-        UH_TRY(make_tmap_bf16(&q64, akv.q, width, T, akv.ld_qkv, 64, fb::BN));
-        UH_TRY(make_tmap_bf16(&dA64, akv.dout, width, T, akv.ld_dout, 64, fb::BN));
-        UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));
-        UH_TRY(make_tmap_bf16(&v128, akv.v, width, T, akv.ld_qkv, 64, 128));
-        UH_TRY(make_tmap_f32(&dqm, akv.dq_acc, width, T, akv.ld_acc, 32, fb::BN));
-        UH_CUDA(cudaMemsetAsync(akv.dq_acc, 0, (size_t)T * akv.ld_acc * sizeof(float), st));
-        UH_CUDA(cudaFuncSetAttribute(fb::attn_bwd_fused_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, fb::SMEM));
-fb::attn_bwd_fused_sm100<<<akv.n_items < sms ? akv.n_items : sms, fb::THREADS, fb::SMEM, st>>>(
-            q64, k128, v128, dA64, dqm, akv);
-        note_launch();
-        UH_CUDA(cudaGetLastError());
-        fb::dq_finish_k<<<4 * sms, 256, 0, st>>>(T, (int)width, akv.dq_acc, akv.ld_acc,
-                                                 (const __nv_bfloat16*)akv.gq, akv.ld_gate, 0.5f * akv.alpha * akv.inv_n,
-                                                 (__nv_bfloat16*)akv.dq, akv.ld_grad);
-        note_launch();
-        UH_CUDA(cudaGetLastError());
-        return UH_OK;
-    }
-    CUtensorMap q128, dA128, k64, v64;
-    UH_TRY(make_tmap_bf16(&q128, aq.q, width, T, aq.ld_qkv, 64, 128));
-    UH_TRY(make_tmap_bf16(&dA128, aq.dout, width, T, aq.ld_dout, 64, 128));
-    UH_TRY(make_tmap_bf16(&k64, aq.k, width, T, aq.ld_qkv, 64, 64));
-    UH_TRY(make_tmap_bf16(&v64, aq.v, width, T, aq.ld_qkv, 64, 64));
-    UH_CUDA(cudaFuncSetAttribute(dq::attn_bwd_dq_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, dq::SMEM));
-    dq::attn_bwd_dq_sm100<<<aq.n_items < sms ? aq.n_items : sms, NUM_THREADS, dq::SMEM, st>>>(q128, k64, v64, dA128, aq);
-    note_launch();
-    UH_CUDA(cudaGetLastError());
-
-    CUtensorMap q32, dA32, k128, v128;   // q / dA boxes of dkv::BN rows
-    UH_TRY(make_tmap_bf16(&q32, akv.q, width, T, akv.ld_qkv, 64, dkv::BN));
-    UH_TRY(make_tmap_bf16(&dA32, akv.dout, width, T, akv.ld_dout, 64, dkv::BN));
+    CUtensorMap q64, dA64, k128, v128, dqm;
+    UH_TRY(make_tmap_bf16(&q64, akv.q, width, T, akv.ld_qkv, 64, fb::BN));
+    UH_TRY(make_tmap_bf16(&dA64, akv.dout, width, T, akv.ld_dout, 64, fb::BN));
     UH_TRY(make_tmap_bf16(&k128, akv.k, width, T, akv.ld_qkv, 64, 128));
     UH_TRY(make_tmap_bf16(&v128, akv.v, width, T, akv.ld_qkv, 64, 128));
-    UH_CUDA(cudaFuncSetAttribute(dkv::attn_bwd_dkv_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, dkv::SMEM));
-    dkv::attn_bwd_dkv_sm100<<<akv.n_items < sms ? akv.n_items : sms, NUM_THREADS, dkv::SMEM, st>>>(q32, k128, v128, dA32, akv);
+    UH_TRY(make_tmap_f32(&dqm, akv.dq_acc, width, T, akv.ld_acc, 32, fb::BN));
+    UH_CUDA(cudaMemsetAsync(akv.dq_acc, 0, (size_t)T * akv.ld_acc * sizeof(float), st));
+    UH_CUDA(cudaFuncSetAttribute(fb::attn_bwd_fused_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, fb::SMEM));
+    fb::attn_bwd_fused_sm100<<<akv.n_items < sms ? akv.n_items : sms, fb::THREADS, fb::SMEM, st>>>(
+        q64, k128, v128, dA64, dqm, akv);
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    fb::dq_finish_k<<<4 * sms, 256, 0, st>>>(T, (int)width, akv.dq_acc, akv.ld_acc,
+                                             (const __nv_bfloat16*)akv.gq, akv.ld_gate, 0.5f * akv.alpha * akv.inv_n,
+                                             (__nv_bfloat16*)akv.dq, akv.ld_grad);
     note_launch();
     UH_CUDA(cudaGetLastError());
     return UH_OK;

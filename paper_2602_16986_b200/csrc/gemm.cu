@@ -218,11 +218,11 @@ uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st) {
         return fail(UH_ERR_UNSUPPORTED, "gemm EPI_F32 with mixed majors");
     }
     if (g.a_mn) return fail(UH_ERR_UNSUPPORTED, "gemm bf16-out with MN-major A");
-    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A projections; UH_GEMM_PAIR=1
-    // enables them for MN-major B (f1, f2), =2 for both B majors (also dY); unset / 0: off
-    const char* pe = getenv("UH_GEMM_PAIR");   // read per call (measured equal to single CTAs: off by default)
-    const int pair_mode = pe ? atoi(pe) : 0;
-    const bool pair = wide && (pair_mode >= 2 || (pair_mode == 1 && g.b_mn));
+    // CTA pairs (cta_group::2, 256 x 256 pair tiles) for the K-major-A projections: g.pair = 1
+    // enables them for MN-major B (f1, f2), 2 for both B majors (also dY).  The layer leaves
+    // g.pair at kGemmPairDefault (off: measured equal to single CTAs at cfg3,
+    // profiles/r01_gemm_pair_ab.log); the test hook exercises both.
+    const bool pair = wide && (g.pair >= 2 || (g.pair == 1 && g.b_mn));
     if (g.epi == EPI_SILU) {
         if (pair) {
             if (g.b_mn) return launch_sm100<256, false, true, EPI_SILU, 1, 2>(g, st);

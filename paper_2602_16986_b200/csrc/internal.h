@@ -42,6 +42,7 @@ void note_launch();
 // ------------------------------------------------------------------ GEMM
 // C[M,N] = A[M,K] * B[K,N].  a_mn: A stored [K][M] (else [M][K]); b_mn: B stored
 // [K][N] (else [N][K]).  Epilogue per gemm_sm100.cuh (EPI_BF16 / EPI_SILU / EPI_F32).
+constexpr int kGemmPairDefault = 0;   // compile-time choice of the product path (no runtime dispatch)
 struct GemmDesc {
     int M = 0, N = 0, K = 0;
     const void* A = nullptr; int64_t lda = 0; bool a_mn = false;
@@ -52,6 +53,7 @@ struct GemmDesc {
     const float* bias = nullptr;
     const void* resid = nullptr; int64_t ldr = 0;
     float* colsum = nullptr;   // EPI_F32 only: += column sums of B (fused bias gradient)
+    int pair = kGemmPairDefault;   // cta_group::2 pair tiles: 0 off, 1 MN-major B only, 2 both majors
 };
 uh_status gemm_run(const GemmDesc& g, uh_dtype dt, cudaStream_t st);
 // NEXT-2: D = diag(sa) (A B) diag(sb) (+ bias)(+ resid) with A [M,K] and B^T [N,K] E4M3, K-major,

@@ -14,8 +14,8 @@ constexpr int kSegs = 256;  // segments per launch (kernel-parameter budget)
 struct Seg { int32_t src, dst, len; };
 struct SegBatch { Seg s[kSegs]; int n; };
 
-// copy `len` rows per segment with VT-wide vectors (uint4: row bytes multiple of 16; uint2:
-// multiple of 8, e.g. int64 timestamps)
+// copy `len` rows per segment with VT-wide vectors (uint4: row bytes and both strides multiples of
+// 16; uint2: multiples of 8, e.g. int64 timestamps or an odd 8-byte stride)
 template <typename VT>
 __global__ void __launch_bounds__(256) copy_rows_k(SegBatch b, const uint8_t* __restrict__ x, int64_t ldx_bytes,
                                                    uint8_t* __restrict__ y, int64_t ldy_bytes, int64_t row_bytes) {
@@ -61,9 +61,12 @@ uh_status run_segments(const std::vector<Seg>& segs, const void* x, int64_t ldx_
         b.n = (int)std::min<size_t>(kSegs, segs.size() - i0);
         for (int i = 0; i < b.n; ++i) b.s[i] = segs[i0 + i];
         dim3 grid((unsigned)std::min(64, (maxlen + 7) / 8), (unsigned)b.n);
-        if (zero && row_bytes % 16 == 0) zero_rows_k<uint4><<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
+        // 16-byte vectors only when every row start is 16-byte aligned (row bytes AND both
+        // strides): an 8-byte multiple stride puts every odd row 8 bytes off a 16-byte boundary
+        const bool v16 = row_bytes % 16 == 0 && ldx_bytes % 16 == 0 && ldy_bytes % 16 == 0;
+        if (zero && v16) zero_rows_k<uint4><<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
         else if (zero) zero_rows_k<uint2><<<grid, 256, 0, st>>>(b, (uint8_t*)y, ldy_bytes, row_bytes);
-        else if (row_bytes % 16 == 0)
+        else if (v16)
             copy_rows_k<uint4><<<grid, 256, 0, st>>>(b, (const uint8_t*)x, ldx_bytes, (uint8_t*)y, ldy_bytes, row_bytes);
         else
             copy_rows_k<uint2><<<grid, 256, 0, st>>>(b, (const uint8_t*)x, ldx_bytes, (uint8_t*)y, ldy_bytes, row_bytes);

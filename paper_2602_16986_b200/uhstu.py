@@ -55,7 +55,7 @@ class LayerParams(ctypes.Structure):
 
 class LayerSaved(ctypes.Structure):
     _fields_ = [("attn", ctypes.c_void_p), ("ln1_mean", ctypes.c_void_p), ("ln1_rstd", ctypes.c_void_p),
-                ("ln2_mean", ctypes.c_void_p), ("ln2_rstd", ctypes.c_void_p)]
+                ("ln2_mean", ctypes.c_void_p), ("ln2_rstd", ctypes.c_void_p), ("fingerprint", ctypes.c_uint64)]
 
 
 class LayerGrads(ctypes.Structure):
@@ -102,7 +102,8 @@ def lib():
                   "uh_jagged_to_padded", "uh_padded_to_jagged", "uh_partition_lpt"):
             getattr(L, f).restype = ctypes.c_int
         L.uh_test_gemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, i64, ctypes.c_int, vp, i64,
-                                   ctypes.c_int, ctypes.c_int, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int, vp]
+                                   ctypes.c_int, ctypes.c_int, vp, i64, vp, i64, vp, vp, i64, ctypes.c_int,
+                                   ctypes.c_int, vp]
         L.uh_test_gemm.restype = ctypes.c_int
         L.uh_test_launch_count.restype = ctypes.c_longlong
         # NEXT-2: FP8 projections (include/uhstu_fp8.h)
@@ -231,16 +232,31 @@ def _ws(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
 
 
+def _rows(name: str, *ts) -> int:
+    """The C ABI takes ONE row stride for a group of [T, width] operands (q/k/v, or dq/dk/dv):
+    each must be a 2-D row-major view (unit column stride) and all must share the row stride."""
+    ld = None
+    for t in ts:
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError(f"{name}: expected 2-D row-major views with unit column stride")
+        if ld is not None and t.stride(0) != ld:
+            raise ValueError(f"{name}: all operands must share one row stride (got {ld} and {t.stride(0)})")
+        ld = t.stride(0)
+    return ld
+
+
 def attn_fwd(jag: JaggedBatch, m: Mask, desc: Attn, q, k, v, out=None, ws=None):
     """A = attention(Q, K, V) for the jagged batch; q/k/v may be column views of one buffer."""
     dt = _dtype_code(q)
+    ld_qkv = _rows("q/k/v", q, k, v)
     width = desc.num_heads * desc.head_dim
     if out is None:
         out = torch.empty(q.shape[0], width, dtype=q.dtype, device=q.device)
     d = desc.c()
     if ws is None:
         ws = _ws(attn_workspace_bytes(jag, m, desc, dt, False), q.device)
-    _check(lib().uh_attn_fwd(ctypes.byref(jag.c), m, ctypes.byref(d), dt, _ptr(q), _ptr(k), _ptr(v), q.stride(0),
+    _rows("out", out)
+    _check(lib().uh_attn_fwd(ctypes.byref(jag.c), m, ctypes.byref(d), dt, _ptr(q), _ptr(k), _ptr(v), ld_qkv,
                              _ptr(out), out.stride(0), _ptr(ws), ws.numel(), _stream()))
     return out
 
@@ -261,12 +277,14 @@ def attn_bwd(jag: JaggedBatch, m: Mask, desc: Attn, q, k, v, dout, dq=None, dk=N
         dpos = torch.zeros_like(desc.pos_bias)
     if dts is None and desc.time_bias is not None:
         dts = torch.zeros_like(desc.time_bias)
-    assert dq.stride(0) == dk.stride(0) == dv.stride(0)
+    ld_qkv = _rows("q/k/v", q, k, v)
+    ld_grad = _rows("dq/dk/dv", dq, dk, dv)
+    _rows("dout", dout)
     d = desc.c()
     if ws is None:
         ws = _ws(attn_workspace_bytes(jag, m, desc, dt, True), q.device)
-    _check(lib().uh_attn_bwd(ctypes.byref(jag.c), m, ctypes.byref(d), dt, _ptr(q), _ptr(k), _ptr(v), q.stride(0),
-                             _ptr(dout), dout.stride(0), _ptr(dq), _ptr(dk), _ptr(dv), dq.stride(0),
+    _check(lib().uh_attn_bwd(ctypes.byref(jag.c), m, ctypes.byref(d), dt, _ptr(q), _ptr(k), _ptr(v), ld_qkv,
+                             _ptr(dout), dout.stride(0), _ptr(dq), _ptr(dk), _ptr(dv), ld_grad,
                              _ptr(dpos), _ptr(dts), _ptr(ws), ws.numel(), _stream()))
     return dq, dk, dv, dpos, dts
 
@@ -297,10 +315,11 @@ class Saved:
     ln1_rstd: torch.Tensor
     ln2_mean: torch.Tensor
     ln2_rstd: torch.Tensor
+    fingerprint: int = 0   # written by the forward, checked by the backward (uh_layer_saved)
 
     def c(self) -> LayerSaved:
         return LayerSaved(_ptr(self.attn), _ptr(self.ln1_mean), _ptr(self.ln1_rstd), _ptr(self.ln2_mean),
-                          _ptr(self.ln2_rstd))
+                          _ptr(self.ln2_rstd), self.fingerprint)
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (self.attn, self.ln1_mean, self.ln1_rstd,
@@ -334,6 +353,8 @@ def layer_fwd(jag, m, prm: Params, attn: Attn, x, save: bool = True, out=None, w
     sc = saved.c() if saved is not None else None
     _check(lib().uh_layer_fwd(ctypes.byref(jag.c), m, ctypes.byref(p), dt, _ptr(x), _ptr(out),
                               ctypes.byref(sc) if sc is not None else None, _ptr(ws), ws.numel(), _stream()))
+    if saved is not None:
+        saved.fingerprint = int(sc.fingerprint)
     return out, saved
 
 
@@ -399,14 +420,15 @@ def padded_to_jagged(jag: JaggedBatch, y: torch.Tensor):
 
 
 def test_gemm(A, B, a_mn: bool, b_mn: bool, epi: int, M: int, N: int, K: int, bias=None, resid=None,
-              out0=None, out1=None):
+              out0=None, out1=None, cta_pair: int = 0):
     """Test hook (include/uhstu_testing.h): the internal projection GEMM."""
     dt = _dtype_code(A)
     if out0 is None:
         out0 = torch.zeros(M, N, dtype=torch.float32 if epi == 2 else A.dtype, device=A.device)
     _check(lib().uh_test_gemm(M, N, K, _ptr(A), A.stride(0), int(a_mn), _ptr(B), B.stride(0), int(b_mn), epi,
                               _ptr(out0), out0.stride(0), _ptr(out1), 0 if out1 is None else out1.stride(0),
-                              _ptr(bias), _ptr(resid), 0 if resid is None else resid.stride(0), dt, _stream()))
+                              _ptr(bias), _ptr(resid), 0 if resid is None else resid.stride(0), dt, int(cta_pair),
+                              _stream()))
     return out0, out1
 
 
@@ -489,6 +511,8 @@ def layer_fwd_fp8(jag, m, prm: Params, attn: Attn, x, qw, save: bool = False, ou
     st, _keep = qw
     _check(lib().uh_layer_fwd_fp8(ctypes.byref(jag.c), m, ctypes.byref(p), ctypes.byref(st), _ptr(x), _ptr(out),
                                   ctypes.byref(sc) if sc is not None else None, _ptr(ws), ws.numel(), _stream()))
+    if saved is not None:
+        saved.fingerprint = int(sc.fingerprint)
     return out, saved
 
 

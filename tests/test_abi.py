@@ -141,3 +141,51 @@ def test_bench_reference_arm_prints_one_json_line():
     assert d["value"] > 0 and d["unit"] == "tokens/s" and d["n_gpus"] == 1
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def _layer_params_host(H=2, dh=32):
+    p = U.LayerParams()
+    p.attn = U.Attn(H, dh, norm_n=1.0).c()
+    for f in ("ln1_w", "ln1_b", "w1", "ln2_w", "ln2_b", "w2"):
+        setattr(p, f, ctypes.c_void_p(0x1000))
+    p.eps = 1e-6
+    return p
+
+
+def test_layer_bwd_rejects_foreign_saved_set():
+    """A saved set whose fingerprint was not written by a forward with the same batch, mask and
+    descriptor is a CACHE_MISMATCH ("wrong cache variant"), checked before any launch."""
+    L = U.lib()
+    jag = _jag([0, 17])
+    jag.c.offsets = ctypes.c_void_p(0x1000)
+    p = _layer_params_host()
+    g = U.LayerGrads(*[ctypes.c_void_p(0x1000)] * 10)
+    fake = ctypes.c_void_p(0x1000)
+    for fp in (0, 12345):
+        s = U.LayerSaved(fake, fake, fake, fake, fake, fp)
+        st = L.uh_layer_bwd(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(p), U.F32, fake, ctypes.byref(s),
+                            fake, fake, ctypes.byref(g), 0, None, 0, None)
+        assert L.uh_status_string(st).decode() == "UH_ERR_CACHE_MISMATCH"
+
+
+def test_layer_d_limit_checked_before_any_launch():
+    """d above the row kernels' limit is UNSUPPORTED from the argument checks (nothing zeroed)."""
+    L = U.lib()
+    jag = _jag([0, 17])
+    jag.c.offsets = ctypes.c_void_p(0x1000)
+    p = _layer_params_host(H=9, dh=128)   # d = 1152 > 1024 (fp32 build)
+    n = ctypes.c_size_t(0)
+    st = L.uh_layer_workspace_bytes(ctypes.byref(jag.c), U.mask(4, 0), ctypes.byref(p), U.F32, 1, ctypes.byref(n))
+    assert L.uh_status_string(st).decode() == "UH_ERR_UNSUPPORTED"
+
+
+def test_binding_rejects_mismatched_qkv_strides():
+    """The ABI takes one row stride for q/k/v; the binding refuses views that do not share it."""
+    import torch
+    q = torch.zeros(4, 64)
+    k = torch.zeros(4, 128)[:, :64]
+    with pytest.raises(ValueError):
+        U._rows("q/k/v", q, k, q)
+    with pytest.raises(ValueError):
+        U._rows("dout", torch.zeros(64, 4).t())
+    assert U._rows("q/k/v", q, q, q) == 64

@@ -2,8 +2,8 @@
 (include/uhstu_fp8.h) against the oracle (oracle.quant_rows_e4m3 / gemm_fp8 /
 layer_forward_fp8) on identical seeded inputs.
 
-* Weight codes and scales: bit-exact (bf16 inputs are exact in fp32, so both sides
-  take every fp32 step of reading R19 on the same numbers).
+* Weight codes and scales: the oracle quantises by the plain fp64 definition, the kernel
+  in fp32 (R19): scales within 1e-6, codes equal except adjacent-grid near-midpoint cases.
 * Norm + quant codes: the kernel's LayerNorm is fp32, the oracle's fp64 rounded to
   fp32, so a code may differ only where the value sits within fp32 noise of an E4M3
   rounding midpoint; there it must be the adjacent grid value (R19).  Scales 1e-5.
@@ -58,8 +58,8 @@ def test_quant_weight_bit_exact(KN):
     qt, s = U.quant_weight_fp8(W)
     torch.cuda.synchronize()
     oq, os_ = O.quant_weight_e4m3(bf16_np(W))
-    assert np.array_equal(codes_to_f64(qt), oq)
-    assert np.array_equal(s.double().cpu().numpy(), os_)
+    check_codes(codes_to_f64(qt), s.double().cpu().numpy(), oq, os_)
+    assert np.allclose(s.double().cpu().numpy(), os_, rtol=1e-6, atol=0)
 
 
 @pytest.mark.parametrize("T", [1, 7, 1000, 4099])

@@ -25,9 +25,8 @@ RAGGED = [0, 1, 2, 17, 63, 64, 65, 127, 128, 129, 255, 256, 257]
 # walks several tiles (both TMEM accumulators, barrier phase flips)
 @pytest.mark.parametrize("MNK", [(256, 512, 128), (296, 256, 192), (128, 2048, 512), (768, 512, 1024),
                                  (37965, 512, 128)])
-@pytest.mark.parametrize("pair", ["0", "2"])   # UH_GEMM_PAIR=2: CTA-pair (cta_group::2) tiles where eligible
-def test_gemm_bf16_majors(a_mn, b_mn, MNK, pair, monkeypatch):
-    monkeypatch.setenv("UH_GEMM_PAIR", pair)
+@pytest.mark.parametrize("pair", [0, 2])   # 2: CTA-pair (cta_group::2) tiles where eligible
+def test_gemm_bf16_majors(a_mn, b_mn, MNK, pair):
     M, N, K = MNK
     if a_mn and M % 8:
         pytest.skip("MN-major A is stored [K][M]: its row stride M must be a multiple of 8")
@@ -38,18 +37,17 @@ def test_gemm_bf16_majors(a_mn, b_mn, MNK, pair, monkeypatch):
     Ad = (A.t().contiguous() if a_mn else A).cuda()
     Bd = (B.contiguous() if b_mn else B.t().contiguous()).cuda()
     if a_mn:
-        out, _ = U.test_gemm(Ad, Bd, True, b_mn, 2, M, N, K)
+        out, _ = U.test_gemm(Ad, Bd, True, b_mn, 2, M, N, K, cta_pair=pair)
     else:
-        out, _ = U.test_gemm(Ad, Bd, False, b_mn, 0, M, N, K)
+        out, _ = U.test_gemm(Ad, Bd, False, b_mn, 0, M, N, K, cta_pair=pair)
     torch.cuda.synchronize()
     assert rel_inf(to_np(out), ref.numpy()) < (1e-5 if a_mn else 8e-3)
 
 
 @pytest.mark.parametrize("b_mn", [True, False])
 @pytest.mark.parametrize("M", [200, 20000])
-@pytest.mark.parametrize("pair", ["0", "2"])
-def test_gemm_bf16_silu_and_residual_epilogues(b_mn, M, pair, monkeypatch):
-    monkeypatch.setenv("UH_GEMM_PAIR", pair)
+@pytest.mark.parametrize("pair", [0, 2])
+def test_gemm_bf16_silu_and_residual_epilogues(b_mn, M, pair):
     N, K = 512, 256
     g = torch.Generator().manual_seed(1)
     A = torch.randn(M, K, generator=g).bfloat16()
@@ -61,12 +59,12 @@ def test_gemm_bf16_silu_and_residual_epilogues(b_mn, M, pair, monkeypatch):
     out0 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     out1 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     U.test_gemm(A.cuda(), (B if b_mn else B.t()).contiguous().cuda(), False, b_mn, 1, M, N, K, bias=bias.cuda(),
-                out0=out0, out1=out1)
+                out0=out0, out1=out1, cta_pair=pair)
     torch.cuda.synchronize()
     assert rel_inf(to_np(out0), (h * s).numpy()) < 8e-3
     assert rel_inf(to_np(out1), (s * (1 + h * (1 - s))).numpy()) < 8e-3
     out, _ = U.test_gemm(A.cuda(), (B if b_mn else B.t()).contiguous().cuda(), False, b_mn, 0, M, N, K,
-                         bias=bias.cuda(), resid=R.cuda())
+                         bias=bias.cuda(), resid=R.cuda(), cta_pair=pair)
     torch.cuda.synchronize()
     assert rel_inf(to_np(out), (h + R.double()).numpy()) < 8e-3
 
@@ -225,3 +223,21 @@ def test_jagged_gather_slice_padded():
     back = U.padded_to_jagged(jag, pad)
     assert np.array_equal(to_np(back), xn)
     assert float(pad[0, 5:].abs().sum()) == 0.0
+
+
+def test_jagged_gather_odd_8byte_stride():
+    """16-byte rows read from a view whose row stride is an odd multiple of 8 bytes (width 8 bf16,
+    ld 12): every odd row starts 8 bytes off a 16-byte boundary, so the copy must take the
+    8-byte path (a 16-byte vector load there faults)."""
+    lengths = [3, 6, 1, 9]
+    jag = U.JaggedBatch.from_lengths(lengths)
+    base = torch.arange(sum(lengths) * 12, dtype=torch.float32).reshape(-1, 12).to("cuda", torch.bfloat16)
+    x = base[:, :8]
+    assert x.stride(0) == 12
+    y, j2 = U.jagged_gather(jag, [3, 1, 0], x)
+    y2, _ = U.jagged_slice_latest(jag, 2, x)
+    torch.cuda.synchronize()
+    xn, off = to_np(x), jag.host
+    assert np.array_equal(to_np(y), np.concatenate([xn[off[3]:off[4]], xn[off[1]:off[2]], xn[off[0]:off[1]]]))
+    assert np.array_equal(to_np(y2), np.concatenate([xn[off[b + 1] - min(2, L):off[b + 1]]
+                                                     for b, L in enumerate(lengths)]))

@@ -405,6 +405,28 @@ def test_layer_backward_finite_differences():
 # ---------------------------------------------------------------------------
 # partitioner oracle (LPT)
 # ---------------------------------------------------------------------------
+def test_seq_cost_counts_the_step_flops():
+    """seq_cost against an independent count: the layer step's GEMM list written out from
+    their shapes (M x N x K, 2 flops per multiply-add)
+    plus 4 d_h (forward) + 10 d_h (backward, S recomputed) flops per allowed pair and head,
+    the pairs counted by brute force on the dense mask (never the closed form)."""
+    for L, d, H, K1, K2 in [(1, 64, 2, 16, 2), (17, 64, 2, 16, 2), (300, 128, 1, 40, 7), (97, 256, 2, 0, 0),
+                            (64, 64, 2, O.FULL, 0), (257, 64, 4, 128, 129)]:
+        gemms = [(L, 4 * d, d),      # F2: h = x^ W1
+                 (L, d, d),          # F7: Y W2
+                 (L, 4 * d, d),      # B3: remat h = x^ W1
+                 (L, d, d),          # B1: dY = dOut W2^T
+                 (d, d, L),          # B1: dW2 = Y^T dOut
+                 (d, 4 * d, L),      # B5: dW1 = x^T dH
+                 (L, d, 4 * d)]      # B5: dx^ = dH W1^T
+        gemm_flops = sum(2 * M * N * K for M, N, K in gemms)
+        q = np.arange(L)[:, None]
+        k = np.arange(L)[None, :]
+        win = np.ones((L, L), bool) if K1 == O.FULL else (q - k <= K1)
+        pairs = int(((k <= q) & (win | (k < K2))).sum())
+        assert O.seq_cost(L, d, H, K1, K2) == gemm_flops + pairs * H * (4 + 10) * (d // H)
+
+
 def test_partition_lpt_properties():
     import itertools
     lengths = [300, 17, 1000, 1000, 64, 512, 999, 3, 250]

@@ -29,17 +29,18 @@ Wt = W.t().contiguous()                                                       # 
 bias = torch.zeros(4 * d, device="cuda")
 o0 = torch.empty(T, 4 * d, device="cuda", dtype=torch.bfloat16)
 o1 = torch.empty_like(o0)
-tag = "pair=" + os.environ.get("UH_GEMM_PAIR", "1")
+PAIR = int(os.environ.get("PAIR", "0"))
+tag = f"pair={PAIR}"
 for name, B, bmn in (("B MN-major [K,N]", W, True), ("B K-major [N,K]", Wt, False)):
     for outs in (1, 2):
-        ms = t(lambda: U.test_gemm(A, B, False, bmn, 1, T, 4 * d, d, bias=bias, out0=o0, out1=o1 if outs == 2 else None))
+        ms = t(lambda: U.test_gemm(A, B, False, bmn, 1, T, 4 * d, d, bias=bias, out0=o0, out1=o1 if outs == 2 else None, cta_pair=PAIR))
         print(f"{tag} f1 SiLU {name} outputs={outs}: {ms:.3f} ms  {2 * T * d * 4 * d / ms / 1e9:.0f} TFLOP/s", flush=True)
 # f2 (bias + residual epilogue), dY = dOut W2^T (K-major B), dx^ = dH W1^T (K = 4d, K-major B)
 W2 = (torch.randn(d, d, device="cuda") / d ** 0.5).to(torch.bfloat16)
 b2 = torch.zeros(d, device="cuda")
 R = torch.randn(T, d, device="cuda").to(torch.bfloat16)
 O = torch.empty(T, d, device="cuda", dtype=torch.bfloat16)
-ms = t(lambda: U.test_gemm(A, W2, False, True, 0, T, d, d, bias=b2, resid=R, out0=O))
+ms = t(lambda: U.test_gemm(A, W2, False, True, 0, T, d, d, bias=b2, resid=R, out0=O, cta_pair=PAIR))
 print(f"{tag} f2 bias+resid B MN-major: {ms:.3f} ms  {2 * T * d * d / ms / 1e9:.0f} TFLOP/s", flush=True)
 ms = t(lambda: U.test_gemm(A, W2, False, False, 0, T, d, d, out0=O))
 print(f"{tag} dY B K-major: {ms:.3f} ms  {2 * T * d * d / ms / 1e9:.0f} TFLOP/s", flush=True)

@@ -1,0 +1,4 @@
+# time experiment builds (tools/build_exp.py) against the product build: attention fwd/bwd at cfg3
+mkdir -p gpurun_out
+echo "== product"; timeout 600 python tools/attn_time.py 2>&1 | grep "B="
+for e in $(cat tools/exp/LIST); do echo "== exp $e"; UH_LIB=libuhstu_$e.so timeout 600 python tools/attn_time.py 2>&1 | grep "B="; done

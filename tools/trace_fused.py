@@ -1,5 +1,5 @@
 """Timeline of CTA 0 of the fused attention backward (build: tools/build_variant.py trace3 -DUH_TRACE=3).
-usage: trace_fused.py [first_step] [count]"""
+usage: trace_fused.py [first_step] [count] [rab 0/1]"""
 import ctypes, os, sys
 import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -18,7 +18,9 @@ q, k, v = buf[:, 2 * d:3 * d], buf[:, 3 * d:], buf[:, d:2 * d]
 dA = torch.randn(T, d, generator=g).to("cuda", torch.bfloat16)
 pos, ts = synth.rab_tables(cfg)
 t = synth.timestamps(cfg.seed, lengths)
-attn = U.Attn(4, 128, 1.0, float(cfg.N), torch.from_numpy(pos).cuda(), torch.from_numpy(ts).cuda(), torch.from_numpy(t).cuda())
+rab = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+attn = U.Attn(4, 128, 1.0, float(cfg.N), torch.from_numpy(pos).cuda() if rab else None,
+              torch.from_numpy(ts).cuda() if rab else None, torch.from_numpy(t).cuda() if rab else None)
 m = U.mask(1024, 128)
 gb = torch.empty(T, 3 * d, dtype=torch.bfloat16, device="cuda")
 wb = U._ws(U.attn_workspace_bytes(jag, m, attn, U.BF16, True), "cuda")
