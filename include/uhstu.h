@@ -105,9 +105,9 @@ typedef struct {
  * the paper) and are shared by all heads; NULL tables switch them off.
  * norm_n is the 1/N normaliser (R5), alpha the score scale (R6).
  * head_dim in {32, 64, 128} (bf16 tcgen05 kernels require 128; 32/64 run the
- * fp32 verification build only).  time_bias_len <= 32 (buckets of log2 seconds);
- * the bf16 path keeps pos_bias in shared memory / registers and requires
- * pos_bias_len <= 256 (exact relative offsets up to 255, one shared bias beyond).
+ * fp32 verification build only).  time_bias_len <= 32 (buckets of log2 seconds).
+ * pos_bias_len is any P >= 1 (offsets q - k >= P - 1 share the last entry); the bf16
+ * path reads it through an extended copy built in the workspace each call.
  * ------------------------------------------------------------------------- */
 typedef struct {
     int32_t num_heads;

@@ -54,8 +54,6 @@ uh_status check_desc(const uh_attn_desc* d, uh_dtype dt) {
     if (dt == UH_BF16 && d->head_dim != 128) return fail(UH_ERR_UNSUPPORTED, "bf16 path requires head_dim == 128");
     if (!(d->norm_n > 0.f)) return fail(UH_ERR_DOMAIN, "norm_n must be > 0");
     if (d->pos_bias && d->pos_bias_len < 1) return fail(UH_ERR_DOMAIN, "pos_bias_len < 1");
-    if (dt == UH_BF16 && d->pos_bias && d->pos_bias_len > 256)
-        return fail(UH_ERR_UNSUPPORTED, "bf16 path: pos_bias_len must be <= 256 (exact offsets up to 255)");
     if (d->time_bias) {
         if (d->time_bias_len < 1 || d->time_bias_len > 32) return fail(UH_ERR_DOMAIN, "time_bias_len must be in [1,32]");
         if (!d->timestamps) return fail(UH_ERR_NULL, "timestamps required with time_bias");

@@ -105,7 +105,8 @@ int64_t count_items(const uh_jagged* jag, int BMt, int H) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t items_q = 0, counters = 0, dq_acc = 0, total = 0;
+    size_t items_q = 0, counters = 0, pos_ext = 0, dq_acc = 0, total = 0;
+    int pos_ext_len = 0;
 };
 
 int tile_rows(uh_dtype dt) { return dt == UH_BF16 ? 128 : 64; }
@@ -117,6 +118,11 @@ WsLayout ws_layout(const uh_jagged* jag, const uh_attn_desc* desc, uh_dtype dt, 
     size_t off = 0;
     w.items_q = off; off += align256(n * sizeof(WorkItem));
     w.counters = off; off += 256;
+    if (dt == UH_BF16 && desc->pos_bias) {   // two copies of the extended position table (attn_common.cuh)
+        w.pos_ext_len = (jag->max_len + 2 * kPosOff + 3) & ~3;   // copy 1 stays 16-byte aligned
+        w.pos_ext = off;
+        off += align256((size_t)2 * w.pos_ext_len * sizeof(float));
+    }
     if (backward && dt == UH_BF16) {   // fp32 dQ accumulator [T, H dh]
         w.dq_acc = off;
         off += align256((size_t)jag->total_tokens * desc->num_heads * desc->head_dim * sizeof(float));
@@ -130,6 +136,30 @@ WsLayout ws_layout(const uh_jagged* jag, const uh_attn_desc* desc, uh_dtype dt, 
 size_t attn_ws_bytes(const uh_jagged* jag, uh_mask m, const uh_attn_desc* desc, uh_dtype dt, int backward) {
     (void)m;
     return ws_layout(jag, desc, dt, backward).total;
+}
+
+// Extended position table for the tcgen05 epilogues (R7; layout in attn_common.cuh): copy c, index i
+// holds (pos[clamp(i + c - kPosOff, 0, P - 1)] - pos[P - 1]) / 2.
+__global__ void __launch_bounds__(256) rab_ext_k(const float* __restrict__ pos, int P, float* __restrict__ ext, int Lt) {
+    const float far = pos[P - 1];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * Lt; i += gridDim.x * blockDim.x) {
+        const int c = i >= Lt ? 1 : 0;
+        int dd = i - c * Lt + c - kPosOff;
+        dd = dd < 0 ? 0 : (dd > P - 1 ? P - 1 : dd);
+        ext[i] = 0.5f * (pos[dd] - far);
+    }
+}
+
+static uh_status build_pos_ext(const AttnCall& c, const WsLayout& w, AttnArgs& a) {
+    if (!w.pos_ext_len) return UH_OK;
+    a.pos_ext = reinterpret_cast<float*>((uint8_t*)c.ws + w.pos_ext);
+    a.pos_ext_len = w.pos_ext_len;
+    const int n = 2 * w.pos_ext_len;
+    rab_ext_k<<<(n + 255) / 256 < 64 ? (n + 255) / 256 : 64, 256, 0, c.st>>>(a.pos, a.P, const_cast<float*>(a.pos_ext),
+                                                                            w.pos_ext_len);
+    note_launch();
+    UH_CUDA(cudaGetLastError());
+    return UH_OK;
 }
 
 static AttnArgs base_args(const AttnCall& c, uh_dtype dt) {
@@ -174,6 +204,7 @@ uh_status attn_fwd_run(const AttnCall& c, uh_dtype dt) {
     if (a.n_items == 0) return UH_OK;
     UH_TRY(schedule(c, dt, SCHED_Q, (WorkItem*)a.items, a.counter));
     if (dt == UH_F32) return attn_fwd_simt_launch(a, c.st);
+    UH_TRY(build_pos_ext(c, w, a));
     return attn_fwd_sm100_launch(a, c.st, c.jag->total_tokens);
 }
 
@@ -193,6 +224,7 @@ uh_status attn_bwd_run(const AttnCall& c, uh_dtype dt) {
     a.dq_acc = reinterpret_cast<float*>(ws + w.dq_acc);
     a.ld_acc = (int64_t)a.H * a.dh;
     UH_TRY(schedule(c, dt, SCHED_K, (WorkItem*)a.items, a.counter));
+    UH_TRY(build_pos_ext(c, w, a));
     return attn_bwd_sm100_launch(a, c.st, c.jag->total_tokens);
 }
 

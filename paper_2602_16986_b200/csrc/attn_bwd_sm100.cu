@@ -59,13 +59,27 @@ __device__ __forceinline__ void store_out_row64(void* base, int64_t ld, int64_t 
                            pack_bf16(w[ch * 8 + 4], w[ch * 8 + 5]), pack_bf16(w[ch * 8 + 6], w[ch * 8 + 7]));
 }
 
+// sum of 32 fp32 values as a tree of packed FADD2
+__device__ __forceinline__ float sum32_f2(const float* v) {
+    uint64_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fadd2(f2_pack(v[4 * i], v[4 * i + 1]), f2_pack(v[4 * i + 2], v[4 * i + 3]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = fadd2(x[i], x[i + 4]);
+    x[0] = fadd2(x[0], x[2]); x[1] = fadd2(x[1], x[3]);
+    const float2 r = f2_unpack(fadd2(x[0], x[1]));
+    return r.x + r.y;
+}
+
 // ============================================================================ fused kernel
 // One pass per 128-key tile computes dV, dK and the dQ partials of every visible 64-query
 // step: dQ^T = K^T dS^T (SS, M = dh, N = 64) lands in the TMEM columns of the consumed
 // S^T, is read by a fourth warpgroup and added into an fp32 [T, H dh] buffer with TMA
 // reductions (in L2: the schedule's consecutive key tiles keep the touched query rows
-// L2-resident).  S, P and dP are computed once instead of once per kernel.  The same
-// warpgroup reduces d pos_bias / d time_bias from the dS^T tile in shared memory.
+// L2-resident).  S, P and dP are computed once instead of once per kernel.  The rab
+// gradients: d time_bias in the P/dS epilogue from the fp32 dS (per-lane bucket runs,
+// shared atomics), d pos_bias in the dQ warpgroup from the dS^T tile in shared memory
+// (skewed-shuffle diagonal sums, one global reduction per diagonal and warp), any P.
 namespace fb {
 #if UH_TRACE == 3   // per-step timeline of CTA 0 (tools/trace_fused.py)
 #define TRACE_FB(ev, sc) do { if (lane == 0) TRACE((ev) * 1024 + ((sc) & 1023)); } while (0)
@@ -75,15 +89,17 @@ namespace fb {
 constexpr int BM = 128, BN = 64;          // 128 keys (MMA M), 64 queries per step
 constexpr int KT = BM * DH * 2;           // K / V tile (32 KB: 2 x 16 KB blocks of [128 rows x 128 B])
 constexpr int QT = BN * DH * 2;           // Q / dA tile (16 KB: 2 x 8 KB blocks of [64 rows x 128 B])
-constexpr int STAGES = 2;                 // (Q, dA) ring
+constexpr int STAGES = 3;                 // (Q, dA) ring
 constexpr int DS_BYTES = BM * BN * 2;     // dS^T [128 keys][64 queries] bf16, one SW128 block
 constexpr int STG_BYTES = BN * 32 * 4;    // per dQ warp: [64 queries][32 dh] fp32 box
-constexpr int TSL = 4 * 32 * 32 * 4;      // d time_bias partials [4 warps][32 buckets][32 lanes]
 constexpr int THREADS = 512;              // w0 TMA, w1 MMA (S/dP), w2 TMEM alloc, w3 MMA (dV/dK/dQ),
                                           // w4-11 P/dS epilogue, w12-15 dQ + d rab
 constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-constexpr int SMEM_DATA = 2 * KT + STAGES * 2 * QT + 2 * DS_BYTES + 4 * STG_BYTES + TSL + kPosTab * 4 + 256 + 512;
-constexpr int SMEM = SMEM_DATA + 1024;
+constexpr int DTS_LANES = 16;             // d time_bias partials [32 buckets][16 lane slots] (2-way at most)
+constexpr int SMEM_DATA = 2 * KT + STAGES * 2 * QT + 2 * DS_BYTES + 4 * STG_BYTES + 32 * 4 + 32 * DTS_LANES * 4 + 512;
+// dynamic shared memory starts 1024-byte aligned (the CTA's first 1 KB is reserved by the
+// hardware); the kernel traps otherwise, since the SW128 tiles need it
+constexpr int SMEM = SMEM_DATA;
 static_assert(SMEM <= 232448, "fused bwd shared memory");
 
 struct __align__(8) Bars {
@@ -92,7 +108,7 @@ struct __align__(8) Bars {
     uint64_t s_full[2], p_full[2];
     uint64_t dq_full[2];    // dQ^T(i) in the S columns of buffer i & 1
     uint64_t s_free[2];     // ... read by the dQ warps: the next S^T may overwrite them
-    uint64_t ds_free[2];    // dS^T shared buffer read by the dQ MMA and the d rab reduction
+    uint64_t ds_free[2];    // dS^T shared buffer read by the dQ MMA and the d pos_bias reduction
     uint64_t acc_full, acc_empty;
     ItemRing ring;
     uint32_t tmem;
@@ -107,17 +123,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdA,
                      const __grid_constant__ CUtensorMap tmDQ, AttnArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    if (smem_u32(smem_raw) & 1023) __trap();
+    uint8_t* smem = smem_raw;
     uint8_t* sK = smem;                                   // K 32 KB | V 32 KB
     uint8_t* sV = smem + KT;
     uint8_t* sQA = smem + 2 * KT;                         // [STAGES] x (Q 16 KB | dA 16 KB)
     uint8_t* sDS = sQA + STAGES * 2 * QT;                 // [2] x dS^T
     float* sDQ = reinterpret_cast<float*>(sDS + 2 * DS_BYTES);   // [4 warps] x [64][32] fp32
-    float* tsl = sDQ + 4 * STG_BYTES / 4;                 // [4 warps][32 buckets][32 lanes]
-    float* pos_s = tsl + TSL / 4;
-    float* ts_s = pos_s + kPosTab;
-    Bars* bars = reinterpret_cast<Bars*>(ts_s + 64);
+    float* ts_s = sDQ + 4 * STG_BYTES / 4;                // time_bias / 2 [32]
+    float* dts_s = ts_s + 32;                             // d time_bias partials [32 buckets][DTS_LANES]
+    Bars* bars = reinterpret_cast<Bars*>(dts_s + 32 * DTS_LANES);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     TRACE_SETUP();
 
@@ -132,8 +148,8 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         ring_init(&bars->ring, 14);  // MMA warps 1, 3 + 8 P/dS warps + 4 dQ warps
         fence_barrier_init();
     }
-    stage_rab(a, pos_s, ts_s);
-    for (int i = threadIdx.x; i < TSL / 4; i += THREADS) tsl[i] = 0.f;
+    stage_ts(a, ts_s);
+    for (int i = threadIdx.x; i < 32 * DTS_LANES; i += THREADS) dts_s[i] = 0.f;
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
     __syncthreads();
@@ -285,8 +301,22 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             const int n = n_qtiles(k0, L, a.K1, a.K2);
             const int kp = k0 + r;
             const bool kok = kp < L;
-            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const ChunkCtx cx = make_ctx(a, ts_s, o, L);
             const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
+            // d time_bias: buckets are monotone along the key row (sorted timestamps), so the
+            // row's dS' values are summed in registers per run of equal bucket and a run is
+            // added to the CTA's shared partials only when the bucket changes (slot lane % 16 of
+            // the bucket's row: lanes of one flush never share an address)
+            float* const dts_l = dts_s + (lane & (DTS_LANES - 1));
+            int run_b = 0;
+            float run_v = 0.f;
+            auto run_add = [&](int b, float v) {
+                if (b != run_b) {
+                    if (run_v != 0.f) atomicAdd(dts_l + run_b * DTS_LANES, run_v);
+                    run_b = b; run_v = 0.f;
+                }
+                run_v += v;
+            };
             for (int i = 0; i < n; ++i, ++sc) {
                 const int sb = sc & 1;
                 const int qb = (k0 / BN + i) * BN + 32 * wg;   // this warpgroup's 32 queries
@@ -320,6 +350,8 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                     const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
                     const float2 dv = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * c], dp[2 * c + 1]), A1), W));
                     d2[c] = kok ? pack_bf16(dv.x, dv.y) : 0u;   // keys beyond L must not reach dQ
+                    dp[2 * c] = kok ? dv.x : 0.f;                // dp now holds the fp32 dS'
+                    dp[2 * c + 1] = kok ? dv.y : 0.f;
                 }
                 // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
                 tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);
@@ -333,7 +365,25 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
                 if (warp == 4) TRACE_FB(3, sc);
+                if (a.dts) {   // runs of equal time bucket along the row (FLAG_T1: two, FLAG_T2: per element)
+                    if (!(ch.flags & FLAG_T2)) {
+                        float tsum = sum32_f2(dp), so = 0.f;
+                        if (ch.flags & FLAG_T1) {   // columns [n, 32) are in bucket b_other
+                            float m[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) m[j] = j >= ch.n ? dp[j] : 0.f;
+                            so = sum32_f2(m);
+                        }
+                        run_add(ch.b_base, tsum - so);
+                        if (ch.n < 32) run_add(ch.b_other, so);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            run_add(bucket32(__shfl_sync(0xffffffffu, ch.tcol, j) - tk, cx.NB), dp[j]);
+                    }
+                }
             }
+            if (run_v != 0.f) atomicAdd(dts_l + run_b * DTS_LANES, run_v);
             mbar_wait_sleep(&bars->acc_full, ki & 1);
             __syncwarp();
             tc_fence_after();
@@ -353,18 +403,19 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             }
         }
     } else if (warp >= 12) {
-        // ============================================================ dQ + d rab
+        // ============================================================ dQ + d pos_bias
         const int wq = warp & 3;
-        const int r = wq * 32 + lane;                       // key row of this thread (d rab)
+        const int r = wq * 32 + lane;                       // key row of this thread (d pos_bias)
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;   // TMEM lanes = dh [32 wq, 32 wq + 32)
         float* stg = sDQ + wq * (STG_BYTES / 4);
-        const bool rab = a.dpos || a.dts;
         const float rscale = 0.5f * a.inv_n;                // ds = rscale * ds'
-        float far_acc = 0.f;
-        float dpr[kMaxNearT];
-#pragma unroll
-        for (int t = 0; t < kMaxNearT; ++t) dpr[t] = 0.f;
-        float* const tsl_l = tsl + wq * 1024 + lane;
+        constexpr int kNoCarry = INT_MIN;
+        float far_acc = 0.f;                                // sum of ds' at offsets >= P - 1 (this lane)
+        auto emit_pos = [&](int dd, float v) {
+            if (dd < 0 || v == 0.f) return;
+            if (dd >= a.P - 1) far_acc += v;
+            else atomicAdd(a.dpos + dd, v * rscale);
+        };
         int sc = 0, ki = 0;
         for (;; ++ki) {
             const int w = ring_take(&bars->ring, ki, lane);
@@ -373,10 +424,8 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int k0 = it.tile * BM;
             const int n = n_qtiles(k0, L, a.K1, a.K2);
-            const int kp = k0 + r;
-            const bool kok = kp < L;
-            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
-            const int32_t tk = (a.ts && kok) ? rel32(__ldg(a.t + o + kp), cx.t0) : 0;
+            float carry = 0.f;                              // lane's pending diagonal sum at carryC + lane
+            int carryC = kNoCarry;
             for (int i = 0; i < n; ++i, ++sc) {
                 const int sb = sc & 1;
                 const int qb0 = (k0 / BN + i) * BN;
@@ -402,120 +451,71 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                     tma_reduce_add_2d(&tmDQ, stg, h * DH + 32 * wq, o + qb0);
                     bulk_commit();
                 }
-                if (rab) {
+                if (a.dpos) {
+                    // d pos_bias[min(q - k, P - 1)] += ds: in this warp's 32 x 32 block of dS^T the
+                    // element (row s, column c) sits on diagonal C + c - s; a skewed shuffle (lane m
+                    // reads column c from lane (c - m) mod 32) gives lane m the sums of diagonals
+                    // C + m (c >= m) and C + m - 32 (c < m).  Consecutive blocks of a warp step C by
+                    // 32, so the second sum completes the first of the previous block: one global
+                    // reduction per lane and block; offsets >= P - 1 accumulate in a register.
                     mbar_wait(&bars->p_full[sb], (sc >> 1) & 1);   // the P/dS warps' shared stores are visible
                     const uint8_t* row = sDS + sb * DS_BYTES + r * 128;
 #pragma unroll 1
                     for (int hf = 0; hf < 2; ++hf) {
-                        const int qb = qb0 + 32 * hf;
-                        const int32_t tcur = col_time(cx, qb, lane);
-                        const Chunk ch = k_chunk(cx, kp, kok, tk, qb, tcur);
+                        const int C = qb0 + 32 * hf - k0 - 32 * wq;
+                        if (C + 31 < 0) continue;                  // warp-uniform: strictly upper (masked)
                         uint32_t d2[16];
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const uint4 u = *reinterpret_cast<const uint4*>(row + (((4 * hf + c) ^ (r & 7)) << 4));
                             d2[4 * c] = u.x; d2[4 * c + 1] = u.y; d2[4 * c + 2] = u.z; d2[4 * c + 3] = u.w;
                         }
-                        const float tsum = sum_packed16(d2);   // rows beyond L carry zeros
-                        if (a.dts) {
-                            if (!(ch.flags & FLAG_T2)) {
-                                float so = 0.f;                // columns [n, 32) are in bucket b_other (FLAG_T1)
-                                if ((ch.flags & FLAG_T1) && ch.n < 32) {
-                                    uint32_t m2[16];
-#pragma unroll
-                                    for (int e = 0; e < 16; ++e)
-                                        m2[e] = d2[e] & (2 * e >= ch.n ? 0xFFFFFFFFu : (2 * e + 1 >= ch.n ? 0xFFFF0000u : 0u));
-                                    so = sum_packed16(m2);
-                                    if (kok) tsl_l[ch.b_other * 32] += so;
-                                }
-                                if (kok) tsl_l[ch.b_base * 32] += tsum - so;
-                            } else {                           // next to the diagonal: per-element buckets,
-                                int bk[32];                    // monotone along the row (runs flushed on change)
-#pragma unroll
-                                for (int c = 0; c < 32; ++c) bk[c] = bucket32(__shfl_sync(0xffffffffu, ch.tcol, c) - tk, cx.NB);
-                                if (kok) {
-                                    int cur = bk[0];
-                                    float acc = 0.f;
-#pragma unroll
-                                    for (int c = 0; c < 32; ++c) {
-                                        const float2 u = unpack_bf16x2(d2[c >> 1]);
-                                        if (bk[c] != cur) { tsl_l[cur * 32] += acc; cur = bk[c]; acc = 0.f; }
-                                        acc += (c & 1) ? u.y : u.x;
-                                    }
-                                    tsl_l[cur * 32] += acc;
-                                }
-                            }
+                        if (C - 31 >= a.P - 1) {                   // warp-uniform: every offset clamps to P - 1
+                            far_acc += sum_packed16(d2);
+                            if (carryC != kNoCarry) emit_pos(carryC + lane, carry);
+                            carryC = kNoCarry;
+                            continue;
                         }
-                        far_acc += tsum;
-                        // near diagonals: delta = q - k = C + c - lane with C a multiple of 32; a
-                        // skewed shuffle gives lane m the sums of diagonals C + m and C + m - 32
-                        if (a.dpos) {
-                            const int C = qb - k0 - 32 * wq;
-                            if (C >= -31 && C <= a.P + 29) {   // warp-uniform
-                                float lo_s = 0.f, hi_s = 0.f;
+                        float tot = 0.f, pre = 0.f;
 #pragma unroll
-                                for (int c = 0; c < 32; ++c) {
-                                    const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (c - lane) & 31));
-                                    const float xv = (c & 1) ? u.y : u.x;
-                                    if (c >= lane) lo_s += xv; else hi_s += xv;
-                                }
-                                const int dlo = C + lane, dhi = C + lane - 32;
-                                const bool ok_lo = dlo >= 0 && dlo <= a.P - 2, ok_hi = dhi >= 0 && dhi <= a.P - 2;
-                                const int tlo = C >> 5;   // diagonal C + lane = lane + 32 * tlo
-#pragma unroll
-                                for (int t = 0; t < kMaxNearT; ++t) {
-                                    dpr[t] += (ok_lo && t == tlo) ? lo_s : 0.f;
-                                    dpr[t] += (ok_hi && t == tlo - 1) ? hi_s : 0.f;
-                                }
-                                far_acc -= (ok_lo ? lo_s : 0.f) + (ok_hi ? hi_s : 0.f);
-                            }
+                        for (int c = 0; c < 32; ++c) {
+                            const float2 u = unpack_bf16x2(__shfl_sync(0xffffffffu, d2[c >> 1], (c - lane) & 31));
+                            tot += (c & 1) ? u.y : u.x;
+                            if (c + 1 == lane) pre = tot;          // sum over c < m
                         }
+                        if (carryC == C - 32) {
+                            emit_pos(C - 32 + lane, pre + carry);
+                        } else {
+                            if (carryC != kNoCarry) emit_pos(carryC + lane, carry);
+                            emit_pos(C - 32 + lane, pre);
+                        }
+                        carry = tot - pre;
+                        carryC = C;
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_free[sb]);
                 if (warp == 12) TRACE_FB(6, sc);
             }
+            if (a.dpos && carryC != kNoCarry) emit_pos(carryC + lane, carry);
         }
         if (lane == 0) bulk_wait0();
         __syncwarp();
-        // ---- CTA-level reduction of the d rab partials, then one global atomic per entry
-        if (rab) {
-            const int et = threadIdx.x - 384;                    // 0..127 among the dQ warps
-            float* redp = sDQ;                                   // [kMaxNearT*32][4 warps] + far[4]
-            named_bar_sync(3, 128);                              // every warp's last TMA add has read its box
-            if (a.dpos) {
+        if (a.dpos) {   // the far entry: one atomic per warp
 #pragma unroll
-                for (int t = 0; t < kMaxNearT; ++t) redp[(t * 32 + lane) * 4 + wq] = dpr[t];
-            }
-            float f = far_acc;
+            for (int off = 16; off > 0; off >>= 1) far_acc += __shfl_xor_sync(0xffffffffu, far_acc, off);
+            if (lane == 0 && far_acc != 0.f) atomicAdd(a.dpos + a.P - 1, far_acc * rscale);
+        }
+    }
+    if (warp >= 4 && warp < 12) {
+        // the CTA's d time_bias partials -> one global atomic per bucket
+        named_bar_sync(4, 256);
+        const int t = threadIdx.x - 128;
+        if (a.dts && t < a.NB) {
+            float v = 0.f;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
-            if (lane == 0) redp[kMaxNearT * 32 * 4 + wq] = f;
-            named_bar_sync(3, 128);
-            if (a.dts) {                       // bucket et >> 2, warp et & 3: 32 lanes, then 4 warps
-                const int b = et >> 2, w4 = et & 3;
-                float sum = 0.f;
-#pragma unroll 8
-                for (int l = 0; l < 32; ++l) sum += tsl[(w4 * 32 + b) * 32 + l];
-                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-                if (w4 == 0 && b < a.NB && sum != 0.f) atomicAdd(a.dts + b, sum * rscale);
-            }
-            if (a.dpos) {
-                for (int e = et; e < a.P - 1; e += 128) {
-                    float sum = 0.f;
-#pragma unroll
-                    for (int w4 = 0; w4 < 4; ++w4) sum += redp[e * 4 + w4];
-                    if (sum != 0.f) atomicAdd(a.dpos + e, sum * rscale);
-                }
-                if (et == 0) {
-                    float sum = 0.f;
-#pragma unroll
-                    for (int w4 = 0; w4 < 4; ++w4) sum += redp[kMaxNearT * 32 * 4 + w4];
-                    if (sum != 0.f) atomicAdd(a.dpos + a.P - 1, sum * rscale);
-                }
-            }
+            for (int l = 0; l < DTS_LANES; ++l) v += dts_s[t * DTS_LANES + l];
+            if (v != 0.f) atomicAdd(a.dts + t, v * (0.5f * a.inv_n));
         }
     }
     __syncthreads();

@@ -39,6 +39,7 @@ struct AttnArgs {
     float alpha, inv_n;
     int K1, K2;  // K1 = INT32_MAX => full causal
     const float* pos; int P;
+    const float* pos_ext; int pos_ext_len;  // bf16 path: two copies of the extended position table (rab_ext_*)
     const float* ts; int NB;
     const int64_t* t;
     const void *q, *k, *v; int64_t ld_qkv;
@@ -122,13 +123,14 @@ UH_HD int query_end(int k0, int rows, int L, int K1, int K2) {
 // ----------------------------------------------------------------------------
 // 32-column chunks of a score tile, seen by one thread-row (tcgen05 epilogues).
 //
-// The epilogue budget is ~8 lane-ops per score element at full tensor rate, so
+// The epilogue budget is a few lane-ops per score element at full tensor rate, so
 // the mask and the rab bias are resolved per 32-column chunk and every
 // per-element component is switched on only when some lane of the warp needs it
 // (warp-uniform flags from one redux.or, so no divergence):
 //   FLAG_M   per-element mask (the chunk crosses the diagonal, the band edge, or L)
-//   FLAG_P   per-element position bias (the chunk is within P-1 of the diagonal):
-//            one LDS with an immediate offset from an extended table
+//   FLAG_P   per-element position bias (some element is within P-1 of the diagonal):
+//            pairs of consecutive offsets read as one 8-byte load from the extended
+//            table in global memory (L1-resident), any P (R7)
 //   FLAG_T1  some lane sees two time buckets: the columns of the larger-dt bucket
 //            form a prefix (queries as rows) / suffix (keys as rows) whose length a
 //            5-step binary search over the lanes' column timestamps finds
@@ -138,15 +140,18 @@ UH_HD int query_end(int k0, int rows, int L, int K1, int K2) {
 // silu(x) = h + h tanh(h); tables are pre-halved.  Timestamps are 32-bit offsets
 // from the sequence's first timestamp (a sequence must span < 2^31 s).
 // Rows beyond L are "don't care" (never stored) and never raise a flag.
+//
+// Extended position table (built per call by rab_ext_k, attn.cu): two copies of
+// length Lt = max_len + 2 kPosOff, copy c holding e_c[i] = (pos[clamp(i + c - kPosOff,
+// 0, P-1)] - pos[P-1]) / 2, so offset dd maps to index dd + kPosOff; a lane whose pairs
+// start at an odd index reads copy 1, making every pair load 8-byte aligned.
 // ----------------------------------------------------------------------------
-constexpr int kPosPad = 64;        // extended position table covers dd in [-64, P+31]
-constexpr int kMaxPosSmem = 256;   // bf16 tcgen05 path: pos_bias_len <= 256 (validated)
-constexpr int kMaxNearT = kMaxPosSmem / 32;  // near-diagonal register partials per lane (dQ kernel)
-constexpr int kPosTab = kMaxPosSmem + 96;
+constexpr int kPosOff = 128;       // extended table covers dd in [-kPosOff, max_len + kPosOff)
 enum { FLAG_M = 1, FLAG_P = 2, FLAG_T1 = 4, FLAG_T2 = 8 };
 
 struct ChunkCtx {
-    const float* pos_e;  // smem: pos_e[dd + kPosPad] = (pos[clamp(dd)] - pos[P-1]) / 2, or nullptr
+    const float* pe;     // global: extended table copy 0 at offset kPosOff (pe[dd] for dd >= -kPosOff), or nullptr
+    int Lt;              // length of one copy (copy 1 = pe + Lt)
     float pos_far;       // pos[P-1] / 2
     int P;
     const float* ts_h;   // smem: ts / 2, or nullptr
@@ -196,17 +201,17 @@ UH_DEV int count_le(int32_t v, int32_t x) {
     return lo;
 }
 
-// rows are queries (forward, dQ); columns are keys kb..kb+31 (dt decreasing along the row)
+// rows are queries (forward); columns are keys kb..kb+31 (dt decreasing along the row)
 UH_DEV Chunk q_chunk(const ChunkCtx& c, int qp, bool qok, int32_t tq, int kb, int32_t tcol) {
     Chunk r;
     unsigned f = 0;
     if (!((kb + 31 <= qp) && (qp - kb <= c.K1 || kb + 31 < c.K2))) f |= FLAG_M;
     float hb = 0.f;
     r.bd = 0;
-    if (c.pos_e) {
-        const int d0 = qp - kb;
+    if (c.pe) {
+        const int d0 = qp - kb;                      // offsets d0 - j, j = 0..31
         if (d0 - 31 < c.P - 1) f |= FLAG_P;
-        r.bd = d0 < -32 ? -32 : (d0 > c.P + 31 ? c.P + 31 : d0);
+        r.bd = d0 < -64 ? -64 : (d0 > c.L + 64 ? c.L + 64 : d0);
         hb += c.pos_far;
     }
     r.tcol = tcol;
@@ -234,17 +239,17 @@ UH_DEV Chunk q_chunk(const ChunkCtx& c, int qp, bool qok, int32_t tq, int kb, in
     return r;
 }
 
-// rows are keys (dK/dV); columns are queries qb..qb+31 (dt increasing along the row)
+// rows are keys (backward); columns are queries qb..qb+31 (dt increasing along the row)
 UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int32_t tk, int qb, int32_t tcol) {
     Chunk r;
     unsigned f = 0;
     if (!((qb >= kp) && (qb + 31 < c.L) && (qb + 31 - kp <= c.K1 || kp < c.K2))) f |= FLAG_M;
     float hb = 0.f;
     r.bd = 0;
-    if (c.pos_e) {
-        const int d0 = qb - kp;
+    if (c.pe) {
+        const int d0 = qb - kp;                      // offsets d0 + j, j = 0..31
         if (d0 < c.P - 1) f |= FLAG_P;
-        r.bd = d0 < -64 ? -64 : (d0 > c.P ? c.P : d0);
+        r.bd = d0 < -96 ? -96 : (d0 > c.L + 64 ? c.L + 64 : d0);
         hb += c.pos_far;
     }
     r.tcol = tcol;
@@ -272,25 +277,34 @@ UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int32_t tk, int qb, in
     return r;
 }
 
-// h[j] = (alpha S + rab)/2 for a query-row chunk.  With WANT_BUCKET the per-element
-// time bucket is returned in bk[] when FLAG_T2 is set.
+// 8-byte load of two consecutive extended-table entries (L1-cached, read-only)
+UH_DEV float2 pe_pair(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+
+// h[j] = (alpha S + rab)/2 for a query-row chunk (offsets bd - j).  With WANT_BUCKET the
+// per-element time bucket is returned in bk[] when FLAG_T2 is set.
 template <bool WANT_BUCKET>
 UH_DEV void q_h(const ChunkCtx& c, const Chunk& ch, int32_t tq, const float* s, float* h, int* bk) {
-    if (ch.flags & FLAG_T1) {
+    const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
+    if (ch.flags & FLAG_P) {   // elements (j, j+1) have offsets (bd-j, bd-j-1): one aligned pair at bd-j-1
+        const int i0 = ch.bd - 1 + kPosOff;
+        const float* pe = c.pe - kPosOff + (i0 & 1) * c.Lt + (i0 & ~1);   // copy (i0 & 1), even index
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, j < ch.n ? ch.hbias_o : ch.hbias);
-    } else {   // common chunk: one packed FFMA2 per pair
-        const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
+        for (int j = 0; j < 32; j += 2) {
+            const float2 pp = pe_pair(pe - j);                              // (.x: offset bd-j-1, .y: bd-j)
+            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, fadd2(B2, f2_pack(pp.y, pp.x))));
+            h[j] = v.x; h[j + 1] = v.y;
+        }
+    } else {                   // common chunk: one packed FFMA2 per pair
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
             const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, B2));
             h[j] = v.x; h[j + 1] = v.y;
         }
     }
-    if (ch.flags & FLAG_P) {
-        const float* pe = c.pos_e + kPosPad + ch.bd;
+    if (ch.flags & FLAG_T1) {
+        const float dT = ch.hbias_o - ch.hbias;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] += pe[-j];
+        for (int j = 0; j < 32; ++j) h[j] += j < ch.n ? dT : 0.f;
     }
     if (ch.flags & FLAG_T2) {
         const float tb = c.ts_h[ch.b_base];
@@ -303,23 +317,29 @@ UH_DEV void q_h(const ChunkCtx& c, const Chunk& ch, int32_t tq, const float* s, 
     }
 }
 
-// the same for a key-row chunk (columns are queries)
+// the same for a key-row chunk (columns are queries, offsets bd + j)
 UH_DEV void k_h(const ChunkCtx& c, const Chunk& ch, int32_t tk, const float* s, float* h) {
-    if (ch.flags & FLAG_T1) {
+    const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
+    if (ch.flags & FLAG_P) {   // elements (j, j+1): offsets (bd+j, bd+j+1), one aligned pair at bd+j
+        const int i0 = ch.bd + kPosOff;
+        const float* pe = c.pe - kPosOff + (i0 & 1) * c.Lt + (i0 & ~1);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] = fmaf(s[j], c.ha, j >= ch.n ? ch.hbias_o : ch.hbias);
-    } else {   // common chunk: one packed FFMA2 per pair
-        const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
+        for (int j = 0; j < 32; j += 2) {
+            const float2 pp = pe_pair(pe + j);
+            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, fadd2(B2, f2_pack(pp.x, pp.y))));
+            h[j] = v.x; h[j + 1] = v.y;
+        }
+    } else {
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
             const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, B2));
             h[j] = v.x; h[j + 1] = v.y;
         }
     }
-    if (ch.flags & FLAG_P) {
-        const float* pe = c.pos_e + kPosPad + ch.bd;
+    if (ch.flags & FLAG_T1) {
+        const float dT = ch.hbias_o - ch.hbias;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] += pe[j];
+        for (int j = 0; j < 32; ++j) h[j] += j >= ch.n ? dT : 0.f;
     }
     if (ch.flags & FLAG_T2) {
         const float tb = c.ts_h[ch.b_base];
@@ -394,23 +414,16 @@ UH_DEV float sum_packed16(const uint32_t* v) {
     return (x.x + x.y) + (y.x + y.y);
 }
 
-// Stage the pre-halved rab tables into shared memory (all threads; caller syncs).
-UH_DEV void stage_rab(const AttnArgs& a, float* pos_e, float* ts_h) {
-    if (a.pos) {
-        const float far = __ldg(a.pos + a.P - 1);
-        for (int i = threadIdx.x; i < a.P + 96; i += blockDim.x) {
-            int dd = i - kPosPad;
-            dd = dd < 0 ? 0 : (dd > a.P - 1 ? a.P - 1 : dd);
-            pos_e[i] = 0.5f * (__ldg(a.pos + dd) - far);
-        }
-    }
+// Stage the pre-halved time-bias table into shared memory (all threads; caller syncs).
+UH_DEV void stage_ts(const AttnArgs& a, float* ts_h) {
     if (a.ts)
         for (int i = threadIdx.x; i < a.NB; i += blockDim.x) ts_h[i] = 0.5f * __ldg(a.ts + i);
 }
 
-UH_DEV ChunkCtx make_ctx(const AttnArgs& a, const float* pos_e, const float* ts_h, int o, int L) {
+UH_DEV ChunkCtx make_ctx(const AttnArgs& a, const float* ts_h, int o, int L) {
     ChunkCtx c;
-    c.pos_e = a.pos ? pos_e : nullptr;
+    c.pe = a.pos ? a.pos_ext + kPosOff : nullptr;
+    c.Lt = a.pos_ext_len;
     c.pos_far = a.pos ? 0.5f * __ldg(a.pos + a.P - 1) : 0.f;
     c.P = a.P;
     c.ts_h = a.ts ? ts_h : nullptr;

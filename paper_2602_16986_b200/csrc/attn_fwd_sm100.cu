@@ -39,7 +39,7 @@ constexpr int LAG = NS - 1;             // the MMA issues S(j) LAG tiles ahead o
 constexpr int O_COL = 256;              // TMEM column of the O accumulator
 constexpr int Q_COL = 384;              // TMEM columns of Q (A operand of S = Q K^T), 64 packed columns
 constexpr int NUM_THREADS = 384;
-constexpr int SMEM_BYTES = QT + STAGES * 2 * KT + kPosTab * 4 + 256 + 1024 + 512;
+constexpr int SMEM_BYTES = QT + STAGES * 2 * KT + 256 + 1024 + 512;
 
 struct __align__(8) FwdBars {
     uint64_t q_full, q_empty;
@@ -69,8 +69,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
     uint8_t* sKV = smem + QT;                     // [STAGES] x (K 16K | V 16K)
-    float* pos_s = reinterpret_cast<float*>(sKV + STAGES * 2 * KT);
-    float* ts_s = pos_s + kPosTab;
+    float* ts_s = reinterpret_cast<float*>(sKV + STAGES * 2 * KT);   // time_bias / 2 [32]
     FwdBars* bars = reinterpret_cast<FwdBars*>(ts_s + 64);
 
     const int warp = threadIdx.x >> 5;
@@ -85,7 +84,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         ring_init(&bars->ring, 9);   // MMA warp + 8 epilogue warps
         fence_barrier_init();
     }
-    stage_rab(a, pos_s, ts_s);
+    stage_ts(a, ts_s);
     if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmQ); tma_prefetch_desc(&tmK); tma_prefetch_desc(&tmV); }
     if (warp == 2) tmem_alloc<512>(&bars->tmem);
     tc_fence_before();
@@ -224,7 +223,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int n = key_tiles_count(kt);
             const int qp = q0 + r;
             const bool qok = qp < L;
-            const ChunkCtx cx = make_ctx(a, pos_s, ts_s, o, L);
+            const ChunkCtx cx = make_ctx(a, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
             // tiles alternate between the two warpgroups (global tile parity), so one group's
             // MUFU-bound SiLU burst overlaps the other's TMEM traffic and bookkeeping
