@@ -370,7 +370,7 @@ def run_inference(args, rank, world, local_rank):
     device = torch.device("cuda", local_rank)
     L, l_keep, n_sla, n_at = args.seq_len, 1024, 6, 12
     B = max(1, args.tokens // L)
-    cfg = synth.Config("cfg5", [L] * B, H=4, dh=128, K1=1024, K2=128, N=L, seed=5 + rank, pos_len=128)
+    cfg = synth.Config("cfg5", [L] * B, H=4, dh=128, K1=1024, K2=128, N=L, seed=5 + rank)
     d = cfg.d
     x = torch.from_numpy(synth.rows_normal(cfg.seed, cfg.lengths, d, 1.0, 0x61)).to(device, torch.bfloat16)
     pos, ts = synth.rab_tables(cfg)

@@ -118,6 +118,8 @@ void orc_attn_fwd(int B, const int32_t* offsets, int H, int dh,
  * Backward of orc_attn_fwd for upstream gradient dA (stride ldA).  Writes
  * dQ, dK, dV (stride ldG, overwritten) and ACCUMULATES into dpos[P] / dts[NB]
  * (caller zeroes them).  dpos/dts may be NULL when the matching table is NULL.
+ * dpos_abs / dts_abs (nullable) accumulate |ds| per entry: the sum of the absolute
+ * terms, the scale of the summation error bound for these cancelling sums (reading R15b).
  */
 void orc_attn_bwd(int B, const int32_t* offsets, int H, int dh,
                   const double* Q, const double* K, const double* V, int64_t ld,
@@ -126,13 +128,15 @@ void orc_attn_bwd(int B, const int32_t* offsets, int H, int dh,
                   const double* pos_w, int64_t P, const double* ts_w, int64_t NB,
                   const int64_t* t,
                   double* dQ, double* dK, double* dV, int64_t ldG,
-                  double* dpos, double* dts, int64_t* work) {
+                  double* dpos, double* dts, double* dpos_abs, double* dts_abs, int64_t* work) {
     int nthr = 1;
 #ifdef _OPENMP
     nthr = omp_get_max_threads();
 #endif
     double* dpos_t = (pos_w && dpos) ? (double*)calloc((size_t)nthr * (size_t)P, sizeof(double)) : NULL;
     double* dts_t = (ts_w && dts) ? (double*)calloc((size_t)nthr * (size_t)NB, sizeof(double)) : NULL;
+    double* dpos_at = (pos_w && dpos_abs) ? (double*)calloc((size_t)nthr * (size_t)P, sizeof(double)) : NULL;
+    double* dts_at = (ts_w && dts_abs) ? (double*)calloc((size_t)nthr * (size_t)NB, sizeof(double)) : NULL;
     int64_t total_work = 0;
 
     /* zero the gradient rows of every sequence (only real rows are touched) */
@@ -173,6 +177,8 @@ void orc_attn_bwd(int B, const int32_t* offsets, int H, int dh,
                     }
                     if (dpos_t) dpos_t[(size_t)tid * P + pos_index(p - pk, P)] += ds;
                     if (dts_t) dts_t[(size_t)tid * NB + time_bucket(t[rq] - t[rk], NB)] += ds;
+                    if (dpos_at) dpos_at[(size_t)tid * P + pos_index(p - pk, P)] += fabs(ds);
+                    if (dts_at) dts_at[(size_t)tid * NB + time_bucket(t[rq] - t[rk], NB)] += fabs(ds);
                 }
             }
         }
@@ -180,9 +186,13 @@ void orc_attn_bwd(int B, const int32_t* offsets, int H, int dh,
     for (int i = 0; i < nthr; ++i) {
         if (dpos_t) for (int64_t j = 0; j < P; ++j) dpos[j] += dpos_t[(size_t)i * P + j];
         if (dts_t) for (int64_t j = 0; j < NB; ++j) dts[j] += dts_t[(size_t)i * NB + j];
+        if (dpos_at) for (int64_t j = 0; j < P; ++j) dpos_abs[j] += dpos_at[(size_t)i * P + j];
+        if (dts_at) for (int64_t j = 0; j < NB; ++j) dts_abs[j] += dts_at[(size_t)i * NB + j];
     }
     free(dpos_t);
     free(dts_t);
+    free(dpos_at);
+    free(dts_at);
     if (work) *work = total_work;
 }
 

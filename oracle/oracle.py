@@ -76,7 +76,7 @@ def _load():
         _lib.orc_attn_bwd.argtypes = [ctypes.c_int, i32p, ctypes.c_int, ctypes.c_int,
                                       dp, dp, dp, I64, dp, I64, I64, I64, D, D,
                                       dp, I64, dp, I64, i64p,
-                                      dp, dp, dp, I64, dp, dp, i64p]
+                                      dp, dp, dp, I64, dp, dp, dp, dp, i64p]
         _lib.orc_attn_bwd.restype = None
         _lib.orc_num_threads.restype = ctypes.c_int
     return _lib
@@ -148,8 +148,10 @@ def attention_forward(offsets, H, dh, q, k, v, spec: AttnSpec, return_work=False
     return (A, int(work.value)) if return_work else A
 
 
-def attention_backward(offsets, H, dh, q, k, v, dA, spec: AttnSpec, return_work=False):
-    """(dQ, dK, dV, dpos, dts) — exact gradient of attention_forward."""
+def attention_backward(offsets, H, dh, q, k, v, dA, spec: AttnSpec, return_work=False, return_abs=False):
+    """(dQ, dK, dV, dpos, dts) — exact gradient of attention_forward.  With return_abs also
+    (dpos_abs, dts_abs): the sums of |ds| per table entry, the scale of the summation error
+    bound of these cancelling sums (reading R15b)."""
     lib = _load()
     offsets = np.ascontiguousarray(offsets, dtype=np.int32)
     B = len(offsets) - 1
@@ -161,6 +163,8 @@ def attention_backward(offsets, H, dh, q, k, v, dA, spec: AttnSpec, return_work=
     ts = _f64(spec.ts_w)
     dpos = None if pos is None else np.zeros(len(pos))
     dts = None if ts is None else np.zeros(len(ts))
+    dpos_abs = None if (pos is None or not return_abs) else np.zeros(len(pos))
+    dts_abs = None if (ts is None or not return_abs) else np.zeros(len(ts))
     t = None
     if ts is not None:
         t = np.ascontiguousarray(spec.timestamps, dtype=np.int64)
@@ -173,8 +177,9 @@ def attention_backward(offsets, H, dh, q, k, v, dA, spec: AttnSpec, return_work=
                      _ptr(ts, ctypes.c_double), 0 if ts is None else len(ts),
                      _ptr(t, ctypes.c_int64),
                      _ptr(dQ, ctypes.c_double), _ptr(dK, ctypes.c_double), _ptr(dV, ctypes.c_double), H * dh,
-                     _ptr(dpos, ctypes.c_double), _ptr(dts, ctypes.c_double), ctypes.byref(work))
-    out = (dQ, dK, dV, dpos, dts)
+                     _ptr(dpos, ctypes.c_double), _ptr(dts, ctypes.c_double),
+                     _ptr(dpos_abs, ctypes.c_double), _ptr(dts_abs, ctypes.c_double), ctypes.byref(work))
+    out = (dQ, dK, dV, dpos, dts) + ((dpos_abs, dts_abs) if return_abs else ())
     return (out, int(work.value)) if return_work else out
 
 
@@ -245,11 +250,12 @@ def layer_forward(x, offsets, prm: LayerParams, H: int, spec: AttnSpec):
     return out, cache
 
 
-def layer_backward(dout, offsets, prm: LayerParams, H: int, spec: AttnSpec, cache=None, x=None):
+def layer_backward(dout, offsets, prm: LayerParams, H: int, spec: AttnSpec, cache=None, x=None, rab_abs=False):
     """Exact gradient of layer_forward for the loss sum(dout * out).
 
     Returns (dx, grads) with grads keys ln1_w, ln1_b, w1, b1, ln2_w, ln2_b, w2, b2,
-    pos_w, ts_w.  Parameter gradients are sums over all tokens."""
+    pos_w, ts_w (with rab_abs also pos_w_abs, ts_w_abs: the sums of |ds| per entry, R15b).
+    Parameter gradients are sums over all tokens."""
     if cache is None:
         _, cache = layer_forward(x, offsets, prm, H, spec)
     dout = _f64(dout)
@@ -262,8 +268,11 @@ def layer_backward(dout, offsets, prm: LayerParams, H: int, spec: AttnSpec, cach
     dAh = dY * c["U"]                                           # gated_norm_backward
     dU = dY * c["Ah"]
     dA, g["ln2_w"], g["ln2_b"] = layer_norm_backward(dAh, c["A"], c["mu2"], c["rs2"], _f64(prm.ln2_w))
-    dQ, dK, dV, g["pos_w"], g["ts_w"] = attention_backward(      # attention_backward
-        offsets, H, d // H, c["Q"], c["K"], c["V"], dA, spec)
+    ab = attention_backward(                                    # attention_backward
+        offsets, H, d // H, c["Q"], c["K"], c["V"], dA, spec, return_abs=rab_abs)
+    dQ, dK, dV, g["pos_w"], g["ts_w"] = ab[:5]
+    if rab_abs:
+        g["pos_w_abs"], g["ts_w_abs"] = ab[5:]
     dS = np.concatenate([dU, dV, dQ, dK], axis=1)               # duqkv
     dH = dS * silu_grad(c["h"])                                 # silu_backward
     g["w1"] = c["xh"].T @ dH                                    # d_linear_w_1

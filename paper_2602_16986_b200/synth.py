@@ -45,7 +45,7 @@ class Config:
     rab: bool = True
     alpha: float = 1.0
     n_layers: int = 1
-    pos_len: int = 0         # P (0 -> N); perf configs use 128: exact offsets < 127, one shared bias beyond (R7)
+    pos_len: int = 0         # P (0 -> N, the configured max length: every offset of the sequence has its own entry, R7)
     ts_len: int = 32         # NB
 
     @property
@@ -90,12 +90,12 @@ def config(name: str, world: int = 1) -> Config:
         return Config("tiny128", [17, 40, 64], H=2, dh=128, K1=16, K2=2, N=64, seed=0)
     if name == "cfg2":
         return Config("cfg2", lengths_uniform(2, 32, 1024, 4096), H=4, dh=128,
-                      K1=WINDOW_FULL, K2=0, N=4096, seed=2, pos_len=128)
+                      K1=WINDOW_FULL, K2=0, N=4096, seed=2)
     if name == "cfg3":
-        return Config("cfg3", [16384] * 16 * world, H=4, dh=128, K1=1024, K2=128, N=16384, seed=3, pos_len=128)
+        return Config("cfg3", [16384] * 16 * world, H=4, dh=128, K1=1024, K2=128, N=16384, seed=3)
     if name == "cfg4":
         return Config("cfg4", lengths_loguniform_until(4, 512, 16384, world * 262144), H=4, dh=128,
-                      K1=1024, K2=128, N=16384, seed=4, n_layers=18, pos_len=128)
+                      K1=1024, K2=128, N=16384, seed=4, n_layers=18)
     raise KeyError(name)
 
 

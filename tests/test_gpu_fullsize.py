@@ -1,9 +1,9 @@
 """GPU parity at BASELINE.json's full size (cfg3: 16 x 16384 tokens, 4 x 128 heads, SLA
-window 1024 + 128 global, rab on), in the launch configuration bench.py times (the whole
-batch through one call).  Sequences are independent and N is explicit (R5), so
-the rows of a sampled sequence must equal the oracle run on that sequence alone; those
+window 1024 + 128 global, rab on with P = 16384), in the launch configuration bench.py times
+(the whole batch through one call).  Sequences are independent and N is explicit (DESIGN.md
+R5), so the rows of a sampled sequence must equal the oracle run on that sequence alone; those
 rows are compared element by element (per-tensor infinity-norm relative, bf16 bar 2e-2).
-Batch-level sums (parameter / rab gradients) are covered at small sizes elsewhere."""
+Batch-level sums (parameter / rab gradients) are compared on two full 16384-token sequences."""
 import numpy as np
 import pytest
 import torch
@@ -118,3 +118,45 @@ def test_attention_cfg2_full_size_sampled_sequences():
         for name, got, r in zip(("dQ", "dK", "dV"), (dq, dk, dv), ref[:3]):
             e = rel_inf(to_np(got[rows]), r)
             assert e <= TOL, (b, name, e)
+
+
+def test_layer_cfg3_two_sequences_all_gradients():
+    """Parameter and rab gradients at the cfg3 shape (4 x 128 heads, SLA 1024 + 128 global,
+    P = 16384, N = 16384) on two full 16384-token sequences through one call -- the launch
+    configuration of bench.py at 1/8 of its batch: the split-K weight-gradient atomics, the fused
+    bias column sums and the per-CTA d rab reductions all run at full sequence length.  Every
+    gradient (and out, dx) against the oracle."""
+    full = _cfg3()
+    cfg = synth.Config("cfg3x2", [16384, 16384], H=full.H, dh=full.dh, K1=full.K1, K2=full.K2, N=full.N,
+                       seed=full.seed)
+    assert cfg.P == 16384
+    p = synth.layer_params(cfg.d, cfg.seed)
+    x, dout = synth.layer_inputs(cfg)
+    pos, ts = synth.rab_tables(cfg)
+    t = synth.timestamps(cfg.seed, cfg.lengths)
+    f = lambda a: torch.from_numpy(a).cuda()
+    w = lambda a: torch.from_numpy(a).to("cuda", torch.bfloat16)
+    prm = U.Params(f(p["ln1_w"]), f(p["ln1_b"]), w(p["w1"]), f(p["ln2_w"]), f(p["ln2_b"]), w(p["w2"]),
+                   f(p["b1"]), f(p["b2"]))
+    attn = U.Attn(cfg.H, cfg.dh, cfg.alpha, float(cfg.N), f(pos), f(ts), f(t))
+    jag = U.JaggedBatch(cfg.offsets())
+    m = U.mask(cfg.K1, cfg.K2)
+    X = to_dev(x, U.BF16)
+    out, saved = U.layer_fwd(jag, m, prm, attn, X)
+    dx, g = U.layer_bwd(jag, m, prm, attn, X, saved, to_dev(dout, U.BF16))
+    torch.cuda.synchronize()
+    prm_o = O.LayerParams(**{kk: np.asarray(vv, np.float64) for kk, vv in p.items()})
+    spec = O.AttnSpec(K1=cfg.K1, K2=cfg.K2, alpha=cfg.alpha, N=float(cfg.N), pos_w=pos, ts_w=ts, timestamps=t)
+    ref_out, cache = O.layer_forward(x, cfg.offsets(), prm_o, cfg.H, spec)
+    ref_dx, ref_g = O.layer_backward(dout, cfg.offsets(), prm_o, cfg.H, spec, cache=cache, rab_abs=True)
+    assert rel_inf(to_np(out), ref_out) <= TOL
+    assert rel_inf(to_np(dx), ref_dx) <= TOL
+    for k in ("ln1_w", "ln1_b", "w1", "b1", "ln2_w", "ln2_b", "w2", "b2"):
+        e = rel_inf(to_np(g[k]), ref_g[k])
+        assert e <= TOL, (k, e)
+    # d pos_bias / d time_bias sum ds of both signs over up to millions of pairs per entry, so
+    # |sum| can be orders of magnitude below the sum of |terms|; the bar applies to the latter,
+    # the scale of the summation error bound (R15b): |g - r| <= TOL * sum |ds| per entry
+    for k, ok in (("pos_bias", "pos_w"), ("time_bias", "ts_w")):
+        err = np.abs(to_np(g[k]) - ref_g[ok])
+        assert np.all(err <= TOL * ref_g[ok + "_abs"] + 1e-12), (k, float(np.max(err / (ref_g[ok + "_abs"] + 1e-30))))

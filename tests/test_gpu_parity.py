@@ -128,18 +128,23 @@ def run_bwd(case: AttnCase, dtype):
 
 def oracle_bwd(case: AttnCase):
     c = case.cfg
-    return O.attention_backward(c.offsets(), c.H, c.dh, case.q, case.k, case.v, case.dA, case.spec())
+    return O.attention_backward(c.offsets(), c.H, c.dh, case.q, case.k, case.v, case.dA, case.spec(),
+                                return_abs=True)
 
 
 def check_bwd(case, dtype):
     got = run_bwd(case, dtype)
     ref = oracle_bwd(case)
-    names = ["dQ", "dK", "dV", "dpos", "dts"]
-    for n, g, r in zip(names, got, ref):
-        if r is None:
-            continue
+    for n, g, r in zip(["dQ", "dK", "dV"], got[:3], ref[:3]):
         e = rel_inf(g, r)
         assert e <= TOL[dtype], (n, e)
+    # d pos_bias / d time_bias: sums of ds of both signs over many pairs per entry; the bar
+    # applies per entry to the summation-error scale sum |ds| (R15b)
+    for n, g, r, ra in zip(["dpos", "dts"], got[3:5], ref[3:5], ref[5:7]):
+        if r is None:
+            continue
+        err = np.abs(np.asarray(g, np.float64) - r)
+        assert np.all(err <= TOL[dtype] * ra + 1e-12), (n, float(np.max(err / (ra + 1e-30))))
 
 
 def test_attn_bwd_f32_tiny():
@@ -148,11 +153,47 @@ def test_attn_bwd_f32_tiny():
     check_bwd(case, U.F32)
 
 
-@pytest.mark.parametrize("K1,K2", [(16, 2), (127, 129), (synth.WINDOW_FULL, 0)])
+# SURVEY §8(c) parity matrix for the backward (and the forward on the same cases): windows K1
+# in {0, 1, 15, 16, 127, 128, 129, 1024, full}, global prefixes K2 in {0, 1, 2, 127, 128, 129,
+# > K1, >= L} (each K1 with a rotating selection of four), and one jagged batch mixing the
+# ragged tile-boundary lengths with {K1, K1+1, K1+2, K1+K2, K1+K2+1, K1+BM, K1+BM+1} (BM = 128).
+# The position table alternates between a short P (most offsets clamp to P-1) and P >= every
+# length (every offset its own entry).
+K1S = [0, 1, 15, 16, 127, 128, 129, 1024, synth.WINDOW_FULL]
+K2S = [0, 1, 2, 127, 128, 129, "gtK1", "geL"]
+BWD_CASES = []
+for _i, _k1 in enumerate(K1S):
+    for _j in range(4):
+        _k2 = K2S[(2 * _i + _j) % len(K2S)]
+        BWD_CASES.append((_k1, _k2, 40 if (_i + _j) % 2 else 5000))
+
+
+def matrix_case(K1, K2, P, seed):
+    fin = K1 < synth.WINDOW_FULL
+    if K2 == "gtK1":
+        K2 = (K1 + 1) if fin else 300
+    if K2 == "geL":
+        K2 = 4000
+    extra = [K1, K1 + 1, K1 + 2, K1 + K2, K1 + K2 + 1, K1 + 128, K1 + 129] if fin else [700, 1300]
+    lengths = RAGGED + sorted({min(L, 1400) for L in extra if L > 0})
+    return AttnCase(lengths, H=2, dh=128, K1=K1, K2=K2, N=1400.0, P=P, seed=6 + K1 % 97 + 3 * (K2 % 13))
+
+
+@pytest.mark.parametrize("K1,K2,P", BWD_CASES)
 @pytest.mark.parametrize("dtype", [U.BF16, U.F32])
-def test_attn_bwd_ragged(K1, K2, dtype):
-    case = AttnCase(RAGGED + [300], H=2, dh=128, K1=K1, K2=K2, N=300.0, P=40, seed=6)
+def test_attn_bwd_ragged_matrix(K1, K2, P, dtype):
+    case = matrix_case(K1, K2, P, 6)
     check_bwd(case, dtype)
+    assert rel_inf(run_fwd(case, dtype), oracle_fwd(case)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("K1,K2", [(1024, 128), (synth.WINDOW_FULL, 0)])
+def test_attn_position_table_longer_than_sequences(K1, K2):
+    """P = 16384 (the cfg3 reading: one entry per offset up to the max length) on sequences of
+    several hundred tiles: every offset reads its own entry; fwd and bwd against the oracle."""
+    case = AttnCase([3000, 1, 2200, 129], H=2, dh=128, K1=K1, K2=K2, N=16384.0, P=16384, seed=11)
+    assert rel_inf(run_fwd(case, U.BF16), oracle_fwd(case)) <= TOL[U.BF16]
+    check_bwd(case, U.BF16)
 
 
 # ----------------------------------------------------------------------------- layer

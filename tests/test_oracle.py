@@ -440,3 +440,25 @@ def test_partition_lpt_properties():
                for asg in itertools.product(range(3), repeat=len(lengths)))
     assert max(load) <= (4 / 3 - 1 / 9) * best + 1e-9
     assert O.partition_lpt(lengths, 3, 64, 2, 16, 2) == (owner, load)
+
+
+def test_rab_gradient_absolute_sums():
+    """The |ds| sums beside d pos_bias / d time_bias (R15b): never below |sum|, equal to it for a
+    single pair, unchanged when dA flips sign (the sums flip), and both tables add up the same
+    sum of |ds| over all visible pairs (every pair lands in exactly one entry of each)."""
+    cfg = synth.Config("abs", [1, 9, 30], H=2, dh=4, K1=5, K2=2, N=30.0, seed=8, pos_len=12, ts_len=8)
+    q, k, v, dA = synth.attn_inputs(cfg)
+    pos, ts = synth.rab_tables(cfg)
+    t = synth.timestamps(cfg.seed, cfg.lengths)
+    spec = O.AttnSpec(K1=cfg.K1, K2=cfg.K2, alpha=1.0, N=cfg.N, pos_w=pos, ts_w=ts, timestamps=t)
+    r = O.attention_backward(cfg.offsets(), cfg.H, cfg.dh, q, k, v, dA, spec, return_abs=True)
+    dpos, dts, apos, ats = r[3], r[4], r[5], r[6]
+    assert np.all(apos >= np.abs(dpos) - 1e-15) and np.all(ats >= np.abs(dts) - 1e-15)
+    assert abs(apos.sum() - ats.sum()) <= 1e-12 * ats.sum()
+    n = O.attention_backward(cfg.offsets(), cfg.H, cfg.dh, q, k, v, -dA, spec, return_abs=True)
+    assert np.allclose(n[3], -dpos, atol=1e-15) and np.allclose(n[5], apos, rtol=1e-12) and np.allclose(n[6], ats, rtol=1e-12)
+    one = synth.Config("one", [1], H=1, dh=4, K1=0, K2=0, N=1.0, seed=9, pos_len=3, ts_len=4)
+    q1, k1, v1, d1 = synth.attn_inputs(one)
+    s1 = O.AttnSpec(K1=0, K2=0, alpha=1.0, N=1.0, pos_w=pos[:3], ts_w=ts[:4], timestamps=t[:1])
+    r1 = O.attention_backward(one.offsets(), 1, 4, q1, k1, v1, d1, s1, return_abs=True)
+    assert r1[5][0] == abs(r1[3][0]) and r1[6][0] == abs(r1[4][0])
