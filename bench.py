@@ -369,10 +369,28 @@ def run_inference(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     L, l_keep, n_sla, n_at = args.seq_len, 1024, 6, 12
-    B = max(1, args.tokens // L)
+    d = 512
+    if args.tokens > 0:
+        B = max(1, args.tokens // L)
+    else:   # fill the GPU: x + two ping-pong outputs + one layer workspace (+ timestamps) per token
+        probe = U.JaggedBatch.from_lengths([L], device)
+        pw = torch.zeros(1, device=device)
+        pb = lambda n: torch.zeros(n, device=device)
+        prm0 = U.Params(pb(d), pb(d), torch.zeros(d, 4 * d, dtype=torch.bfloat16, device=device), pb(d), pb(d),
+                        torch.zeros(d, d, dtype=torch.bfloat16, device=device), pb(4 * d), pb(d))
+        a0 = U.Attn(4, 128, 1.0, float(L), pb(L), pb(32), torch.zeros(L, dtype=torch.int64, device=device))
+        ws_tok = U.layer_workspace_bytes(probe, U.mask(1024, 128), prm0, a0, U.BF16, False) / L
+        per_tok = ws_tok + 3 * d * 2 + 8
+        free, _ = torch.cuda.mem_get_info(device)
+        B = max(1, int(0.93 * free / per_tok) // L)
+        del probe, pw, prm0, a0
     cfg = synth.Config("cfg5", [L] * B, H=4, dh=128, K1=1024, K2=128, N=L, seed=5 + rank)
-    d = cfg.d
-    x = torch.from_numpy(synth.rows_normal(cfg.seed, cfg.lengths, d, 1.0, 0x61)).to(device, torch.bfloat16)
+    # x ~ N(0, 1) drawn on the device in 1M-row chunks (a GPU-filling batch is tens of GB)
+    x = torch.empty(B * L, d, dtype=torch.bfloat16, device=device)
+    gx = torch.Generator(device=device).manual_seed(cfg.seed)
+    for r0 in range(0, B * L, 1 << 20):
+        r1 = min(B * L, r0 + (1 << 20))
+        x[r0:r1] = torch.randn(r1 - r0, d, generator=gx, device=device).to(torch.bfloat16)
     pos, ts = synth.rab_tables(cfg)
     t = torch.from_numpy(synth.timestamps(cfg.seed, cfg.lengths)).to(device)
     f = lambda a: torch.from_numpy(a).to(device)
@@ -386,9 +404,12 @@ def run_inference(args, rank, world, local_rank):
         m = U.mask(cfg.K1, cfg.K2) if li < n_sla else U.mask()
         layers.append(S.Layer(prm, attn, m))
     jag = U.JaggedBatch(cfg.offsets(), device)
+    ws = U._ws(U.layer_workspace_bytes(jag, U.mask(1024, 128), layers[0].params, layers[0].attn, U.BF16, False),
+               device)
+    bufs = [torch.empty_like(x), torch.empty_like(x)]
 
     def step():
-        S.forward_truncated(jag, x, layers, n_sla, l_keep, norm_n_truncated=float(l_keep))
+        S.forward_truncated(jag, x, layers, n_sla, l_keep, norm_n_truncated=float(l_keep), ws=ws, bufs=bufs)
 
     def barrier():
         if world > 1:
@@ -424,7 +445,9 @@ def run_inference(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"cfg5: {B} sequences x L={L} per GPU ({B * L} tokens), 4 heads x 128, "
-                                   f"{n_sla} SLA layers (1024 + 128 global), latest {l_keep} tokens, {n_at} causal layers",
+                                   f"{n_sla} SLA layers (1024 + 128 global), latest {l_keep} tokens, {n_at} causal layers, "
+                                   f"rab P={L}",
+                       "hbm_used_gb": torch.cuda.max_memory_allocated(device) / 1e9,
                        "parallelism": f"replicas x{world} (no collective)", "seq_len": L},
             "gpu_launches": launches, "clocks": clocks,
             "e2e": None, "e2e_note": "inference inputs (x) stay resident; not measured for cfg5"}
@@ -492,7 +515,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--seq-len", type=int, default=16384, help="cfg5: sequence length (4096, 16384, 65536)")
-    ap.add_argument("--tokens", type=int, default=4 * 1048576, help="cfg5: tokens per GPU")
+    ap.add_argument("--tokens", type=int, default=4 * 1048576,
+                    help="cfg5: tokens per GPU (0: as many as fill the GPU's free memory, BASELINE's cfg5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")

@@ -280,75 +280,65 @@ UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int32_t tk, int qb, in
 // 8-byte load of two consecutive extended-table entries (L1-cached, read-only)
 UH_DEV float2 pe_pair(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
 
-// h[j] = (alpha S + rab)/2 for a query-row chunk (offsets bd - j).  With WANT_BUCKET the
-// per-element time bucket is returned in bk[] when FLAG_T2 is set.
-template <bool WANT_BUCKET>
-UH_DEV void q_h(const ChunkCtx& c, const Chunk& ch, int32_t tq, const float* s, float* h, int* bk) {
-    const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
-    if (ch.flags & FLAG_P) {   // elements (j, j+1) have offsets (bd-j, bd-j-1): one aligned pair at bd-j-1
-        const int i0 = ch.bd - 1 + kPosOff;
-        const float* pe = c.pe - kPosOff + (i0 & 1) * c.Lt + (i0 & ~1);   // copy (i0 & 1), even index
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const float2 pp = pe_pair(pe - j);                              // (.x: offset bd-j-1, .y: bd-j)
-            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, fadd2(B2, f2_pack(pp.y, pp.x))));
-            h[j] = v.x; h[j + 1] = v.y;
-        }
-    } else {                   // common chunk: one packed FFMA2 per pair
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, B2));
-            h[j] = v.x; h[j + 1] = v.y;
-        }
+// h[j] = (alpha S + rab)/2 for a 32-column chunk as one FFMA2 per pair of columns, the pair's
+// bias built in registers: the chunk's constant (pos_far + ts of the base bucket), the other
+// bucket's constant on the columns past the FLAG_T1 split, the position-table pair (FLAG_P), and
+// per-element buckets for FLAG_T2.  Q_ROWS: rows are queries, columns keys kb + j (offsets bd - j,
+// the other bucket on columns [0, n)); else rows are keys, columns queries qb + j (offsets bd + j,
+// the other bucket on columns [n, 32)).
+template <bool Q_ROWS, bool T1, bool P>
+UH_DEV void chunk_h_pairs(const ChunkCtx& c, const Chunk& ch, const float* s, float* h) {
+    const uint64_t A2 = f2_pack(c.ha, c.ha);
+    const float hb = ch.hbias, ho = ch.hbias_o;
+    const float* pe = nullptr;
+    if (P) {   // q rows: pairs (j, j+1) = offsets (bd-j, bd-j-1), one aligned pair at bd-j-1; k rows: at bd+j
+        const int i0 = Q_ROWS ? ch.bd - 1 + kPosOff : ch.bd + kPosOff;
+        pe = c.pe - kPosOff + (i0 & 1) * c.Lt + (i0 & ~1);   // copy (i0 & 1), even index
     }
-    if (ch.flags & FLAG_T1) {
-        const float dT = ch.hbias_o - ch.hbias;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] += j < ch.n ? dT : 0.f;
+    for (int j = 0; j < 32; j += 2) {
+        float b0 = hb, b1 = hb;
+        if (T1) {
+            b0 = (Q_ROWS ? j < ch.n : j >= ch.n) ? ho : hb;
+            b1 = (Q_ROWS ? j + 1 < ch.n : j + 1 >= ch.n) ? ho : hb;
+        }
+        uint64_t B2 = f2_pack(b0, b1);
+        if (P) {
+            const float2 pp = pe_pair(Q_ROWS ? pe - j : pe + j);
+            B2 = fadd2(B2, Q_ROWS ? f2_pack(pp.y, pp.x) : f2_pack(pp.x, pp.y));
+        }
+        const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, B2));
+        h[j] = v.x; h[j + 1] = v.y;
     }
-    if (ch.flags & FLAG_T2) {
+}
+
+template <bool Q_ROWS>
+UH_DEV void chunk_h(const ChunkCtx& c, const Chunk& ch, int32_t trow, const float* s, float* h) {
+    const bool t1 = ch.flags & FLAG_T1, p = ch.flags & FLAG_P;   // warp-uniform
+    if (t1) {
+        if (p) chunk_h_pairs<Q_ROWS, true, true>(c, ch, s, h); else chunk_h_pairs<Q_ROWS, true, false>(c, ch, s, h);
+    } else {
+        if (p) chunk_h_pairs<Q_ROWS, false, true>(c, ch, s, h); else chunk_h_pairs<Q_ROWS, false, false>(c, ch, s, h);
+    }
+    if (ch.flags & FLAG_T2) {   // > 2 buckets in some row: per element, relative to the base bucket's bias
         const float tb = c.ts_h[ch.b_base];
+        const bool multi = !(ch.b_other == ch.b_base + 1 || ch.b_other == ch.b_base);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            const int b = bucket32(tq - __shfl_sync(0xffffffffu, ch.tcol, j), c.NB);
-            if (WANT_BUCKET) bk[j] = b;
-            h[j] += (ch.b_other == ch.b_base + 1 || ch.b_other == ch.b_base) ? 0.f : c.ts_h[b] - tb;
+            const int32_t tc = __shfl_sync(0xffffffffu, ch.tcol, j);
+            const int b = bucket32(Q_ROWS ? trow - tc : tc - trow, c.NB);
+            h[j] += multi ? c.ts_h[b] - tb : 0.f;
         }
     }
 }
 
-// the same for a key-row chunk (columns are queries, offsets bd + j)
+// query-row chunk (forward)
+UH_DEV void q_h(const ChunkCtx& c, const Chunk& ch, int32_t tq, const float* s, float* h) {
+    chunk_h<true>(c, ch, tq, s, h);
+}
+// key-row chunk (backward)
 UH_DEV void k_h(const ChunkCtx& c, const Chunk& ch, int32_t tk, const float* s, float* h) {
-    const uint64_t A2 = f2_pack(c.ha, c.ha), B2 = f2_pack(ch.hbias, ch.hbias);
-    if (ch.flags & FLAG_P) {   // elements (j, j+1): offsets (bd+j, bd+j+1), one aligned pair at bd+j
-        const int i0 = ch.bd + kPosOff;
-        const float* pe = c.pe - kPosOff + (i0 & 1) * c.Lt + (i0 & ~1);
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const float2 pp = pe_pair(pe + j);
-            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, fadd2(B2, f2_pack(pp.x, pp.y))));
-            h[j] = v.x; h[j + 1] = v.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-            const float2 v = f2_unpack(ffma2(f2_pack(s[j], s[j + 1]), A2, B2));
-            h[j] = v.x; h[j + 1] = v.y;
-        }
-    }
-    if (ch.flags & FLAG_T1) {
-        const float dT = ch.hbias_o - ch.hbias;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) h[j] += j >= ch.n ? dT : 0.f;
-    }
-    if (ch.flags & FLAG_T2) {
-        const float tb = c.ts_h[ch.b_base];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const int b = bucket32(__shfl_sync(0xffffffffu, ch.tcol, j) - tk, c.NB);
-            h[j] += (ch.b_other == ch.b_base + 1 || ch.b_other == ch.b_base) ? 0.f : c.ts_h[b] - tb;
-        }
-    }
+    chunk_h<false>(c, ch, tk, s, h);
 }
 
 // Visibility of a 32-column chunk as a bit mask (bit c = column c visible), for FLAG_M

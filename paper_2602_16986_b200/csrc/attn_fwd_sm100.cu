@@ -246,7 +246,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     tmem_ld_wait();
                     // h = (alpha S + rab)/2 in fp32, then packed bf16x2: silu(2h) = h + h tanh(h)
                     float hx[32];
-                    q_h<false>(cx, ch, tq, s, hx, nullptr);
+                    q_h(cx, ch, tq, s, hx);
                     if (ch.flags & FLAG_M) apply_vis(hx, q_vis_bits(cx, qp, qok, kb));   // h = 0 -> P = 0
                     uint32_t pk[16];
 #pragma unroll

@@ -25,12 +25,16 @@ class Layer:
 
 
 def forward_truncated(jag: U.JaggedBatch, x: torch.Tensor, layers: List[Layer], n_full: int, l_keep: int,
-                      norm_n_truncated: Optional[float] = None):
+                      norm_n_truncated: Optional[float] = None, ws: Optional[torch.Tensor] = None,
+                      bufs: Optional[List[torch.Tensor]] = None):
     """Forward-only stack (inference, nothing saved).  Returns (out, jag_out): the output rows of
-    the truncated segment and its jagged batch (the whole batch if n_full == len(layers))."""
+    the truncated segment and its jagged batch (the whole batch if n_full == len(layers)).
+    ``ws`` (one layer workspace) and ``bufs`` (two [T, d] ping-pong outputs) may be passed so a
+    batch that fills the GPU allocates nothing per layer."""
     h = x
-    for lay in layers[:n_full]:
-        h, _ = U.layer_fwd(jag, lay.mask, lay.params, lay.attn, h, save=False)
+    for i, lay in enumerate(layers[:n_full]):
+        out = bufs[i % 2] if bufs is not None else None
+        h, _ = U.layer_fwd(jag, lay.mask, lay.params, lay.attn, h, save=False, out=out, ws=ws)
     if n_full == len(layers):
         return h, jag
     h, jt = U.jagged_slice_latest(jag, l_keep, h)
