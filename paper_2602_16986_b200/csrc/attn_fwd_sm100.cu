@@ -112,6 +112,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     const int s = kc % STAGES;
                     uint8_t* st = sKV + s * 2 * KT;
                     mbar_wait_sleep(&bars->kv_empty[s], ((kc / STAGES) & 1) ^ 1);
+                    TRACE(7 * 1024 + (kc & 1023));   // stage free: PV(kc - STAGES) done
                     mbar_arrive_expect_tx(&bars->kv_full[s], 2 * KT);
                     tma_load_2d(st, &tmK, &bars->kv_full[s], h * DH, row);
                     tma_load_2d(st + KT / 2, &tmK, &bars->kv_full[s], h * DH + 64, row);
@@ -264,7 +265,6 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
                 if (warp == 4 && lane == 0) TRACE(5 * 1024 + (sc & 1023));
-                if (warp == 8 && lane == 0) TRACE(7 * 1024 + (sc & 1023));
             }
             // ---- O epilogue: A = O / N
             mbar_wait_sleep(&bars->o_full, qi & 1);

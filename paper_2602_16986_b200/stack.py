@@ -37,9 +37,13 @@ def forward_truncated(jag: U.JaggedBatch, x: torch.Tensor, layers: List[Layer], 
         h, _ = U.layer_fwd(jag, lay.mask, lay.params, lay.attn, h, save=False, out=out, ws=ws)
     if n_full == len(layers):
         return h, jag
-    h, jt = U.jagged_slice_latest(jag, l_keep, h)
+    nxt = None
+    if bufs is not None:   # h lives in bufs[(n_full - 1) % 2]; the truncated rows go to the other one
+        n_keep = int(sum(min(int(L), l_keep) for L in jag.lengths))
+        nxt = [bufs[n_full % 2][:n_keep], bufs[(n_full - 1) % 2][:n_keep]]
+    h, jt = U.jagged_slice_latest(jag, l_keep, h, out=nxt[0] if nxt else None)
     ts_cache = {}
-    for lay in layers[n_full:]:
+    for i, lay in enumerate(layers[n_full:]):
         attn = lay.attn
         if attn.timestamps is not None:
             key = attn.timestamps.data_ptr()
@@ -49,5 +53,6 @@ def forward_truncated(jag: U.JaggedBatch, x: torch.Tensor, layers: List[Layer], 
             attn = replace(attn, timestamps=ts_cache[key])
         if norm_n_truncated is not None:
             attn = replace(attn, norm_n=float(norm_n_truncated))
-        h, _ = U.layer_fwd(jt, lay.mask, lay.params, attn, h, save=False)
+        h, _ = U.layer_fwd(jt, lay.mask, lay.params, attn, h, save=False, out=nxt[(i + 1) % 2] if nxt else None,
+                           ws=ws)
     return h, jt

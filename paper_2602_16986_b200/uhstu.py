@@ -395,9 +395,11 @@ def jagged_gather(jag: JaggedBatch, seq_ids: Sequence[int], x: torch.Tensor):
     return y, JaggedBatch(off, x.device)
 
 
-def jagged_slice_latest(jag: JaggedBatch, l_keep: int, x: torch.Tensor):
+def jagged_slice_latest(jag: JaggedBatch, l_keep: int, x: torch.Tensor, out: Optional[torch.Tensor] = None):
     tot = int(np.minimum(jag.lengths, l_keep).sum())
-    y = torch.empty(tot, x.shape[1], dtype=x.dtype, device=x.device)
+    y = torch.empty(tot, x.shape[1], dtype=x.dtype, device=x.device) if out is None else out
+    if y.shape[0] != tot or y.stride(1) != 1:
+        raise ValueError("jagged_slice_latest: out must hold the kept rows, row-major")
     off = _offsets_out(jag.B)
     _check(lib().uh_jagged_slice_latest(ctypes.byref(jag.c), int(l_keep), _ptr(x), x.stride(0), x.shape[1],
                                         x.element_size(), _ptr(y), off.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
