@@ -179,6 +179,7 @@ static AttnArgs base_args(const AttnCall& c, uh_dtype dt) {
     a.dq = c.dq; a.dk = c.dk; a.dv = c.dv; a.ld_grad = c.ld_grad;
     a.gq = c.gq; a.gk = c.gk; a.gv = c.gv; a.ld_gate = c.ld_gate;
     a.dpos = c.dpos; a.dts = c.dts;
+    a.T = c.jag->total_tokens;
     (void)dt;
     return a;
 }

@@ -173,6 +173,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 const int w = ring_claim_publish(&bars->ring, ki, a.counter, a.n_items);
                 if (w < 0) break;
                 const WorkItem it = a.items[w];
+                check_item(a, it, BM);
                 const int k0 = it.tile * BM, h = it.head & 0xFFFF;
                 const int n = n_qtiles(k0, it.seq_len, a.K1, a.K2);
                 mbar_wait_sleep(&bars->kv_empty, (ki & 1) ^ 1);
@@ -214,6 +215,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 const int w = ring_take(&bars->ring, ki, lane);
                 if (w < 0) break;
                 const WorkItem it = a.items[w];
+                check_item(a, it, BM);
                 const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
                 const uint64_t dk = kv_k, dv = dk + (KT >> 4);
                 mbar_wait(&bars->kv_full, ki & 1);
@@ -256,6 +258,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 const int w = ring_take(&bars->ring, ki, lane);
                 if (w < 0) break;
                 const WorkItem it = a.items[w];
+                check_item(a, it, BM);
                 const int n = n_qtiles(it.tile * BM, it.seq_len, a.K1, a.K2);
                 mbar_wait(&bars->acc_empty, (ki & 1) ^ 1);
                 mbar_wait(&bars->p_full[sc & 1], (sc >> 1) & 1);
@@ -308,6 +311,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             const int w = ring_take(&bars->ring, ki, lane);
             if (w < 0) break;
             const WorkItem it = a.items[w];
+            check_item(a, it, BM);
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int k0 = it.tile * BM;
             const int n = n_qtiles(k0, L, a.K1, a.K2);
@@ -323,6 +327,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
             int run_b = 0;
             float run_v = 0.f;
             auto run_add = [&](int b, float v) {
+                UH_CHECK(b >= 0 && b < a.NB);
                 if (b != run_b) {
                     if (run_v != 0.f) atomicAdd(dts_l + run_b * DTS_LANES, run_v);
                     run_b = b; run_v = 0.f;
@@ -404,6 +409,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 tmem_ld32(tmem + lane_base + DV_COL + wg * 64, acc);
                 tmem_ld32(tmem + lane_base + DV_COL + wg * 64 + 32, acc + 32);
                 tmem_ld_wait();
+                UH_CHECK(!kok || o + kp < a.T);
                 if (kok) store_out_row64(a.dv, a.ld_grad, o + kp, h * DH + wg * 64, acc, a.gv, a.ld_gate, a.inv_n);
                 tmem_ld32(tmem + lane_base + DK_COL + wg * 64, acc);
                 tmem_ld32(tmem + lane_base + DK_COL + wg * 64 + 32, acc + 32);
@@ -437,13 +443,14 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
         auto emit_pos = [&](int dd, float v) {
             if (dd < 0 || v == 0.f) return;
             if (dd >= a.P - 1) far_acc += v;
-            else atomicAdd(a.dpos + dd, v * rscale);
+            else { UH_CHECK(dd >= 0 && dd < a.P - 1); atomicAdd(a.dpos + dd, v * rscale); }
         };
         int sc = 0, ki = 0;
         for (;; ++ki) {
             const int w = ring_take(&bars->ring, ki, lane);
             if (w < 0) break;
             const WorkItem it = a.items[w];
+            check_item(a, it, BM);
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int k0 = it.tile * BM;
             const int n = n_qtiles(k0, L, a.K1, a.K2);
@@ -467,6 +474,7 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                 for (int q = 0; q < 32; ++q) stg[q * 32 + lane] = v[q];
                 fence_proxy_async_smem();
                 __syncwarp();
+                UH_CHECK(qb0 + 32 * hf < L + BN && h < a.H);
                 if (lane == 0) {
                     tma_reduce_add_2d(&tmDQ, stg, h * DH + 32 * wq, o + qb0 + 32 * hf);
                     bulk_commit();

@@ -20,6 +20,15 @@ __device__ long long* g_trace = nullptr;
 #define TRACE(slot) do { } while (0)
 #endif
 
+// Checked builds (-DUH_CHECKED=1, tools/build_variant.py checked): device-side range checks on
+// the work items, table indices, reduction targets and output rows; a violation traps the
+// kernel (compute-sanitizer is not available on the GPU pool, so these are the bounds checks)
+#if UH_CHECKED
+#define UH_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define UH_CHECK(cond) do { } while (0)
+#endif
+
 #define UH_HD __host__ __device__ __forceinline__
 UH_HD int imin(int a, int b) { return a < b ? a : b; }
 UH_HD int imax(int a, int b) { return a > b ? a : b; }
@@ -35,6 +44,7 @@ struct WorkItem {
 struct AttnArgs {
     const WorkItem* items;
     int n_items;
+    int64_t T;                             // total tokens (checked builds)
     int H, dh;
     float alpha, inv_n;
     int K1, K2;  // K1 = INT32_MAX => full causal
@@ -51,6 +61,12 @@ struct AttnArgs {
     float *dpos, *dts;
     int* counter;                          // dynamic work counter (persistent kernels)
 };
+
+// checked builds: a work item lies inside its sequence and the batch
+UH_DEV void check_item(const AttnArgs& a, const WorkItem& it, int rows) {
+    UH_CHECK(it.seq_start >= 0 && it.seq_len > 0 && (int64_t)it.seq_start + it.seq_len <= a.T);
+    UH_CHECK(it.tile >= 0 && it.tile * rows < it.seq_len && (it.head & 0xFFFF) < a.H);
+}
 
 // MMA block order of one item with n tiles whose second block (PV / dQ / dV-dK) runs LAG
 // tiles behind its first (S, or S and dP): S0 .. S(LAG-1), then S(j) P(j-LAG) pairs, then
@@ -293,6 +309,7 @@ UH_DEV void chunk_h_pairs(const ChunkCtx& c, const Chunk& ch, const float* s, fl
     const float* pe = nullptr;
     if (P) {   // q rows: pairs (j, j+1) = offsets (bd-j, bd-j-1), one aligned pair at bd-j-1; k rows: at bd+j
         const int i0 = Q_ROWS ? ch.bd - 1 + kPosOff : ch.bd + kPosOff;
+        UH_CHECK(Q_ROWS ? (i0 - 31 >= 0 && i0 + 1 < c.Lt) : (i0 >= 0 && i0 + 33 < c.Lt));
         pe = c.pe - kPosOff + (i0 & 1) * c.Lt + (i0 & ~1);   // copy (i0 & 1), even index
     }
 #pragma unroll

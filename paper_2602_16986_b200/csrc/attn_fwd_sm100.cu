@@ -100,6 +100,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const int w = ring_claim_publish(&bars->ring, qi, a.counter, a.n_items);
                 if (w < 0) break;
                 const WorkItem it = a.items[w];
+                check_item(a, it, BM);
                 const int q0 = it.tile * BM, h = it.head & 0xFFFF;
                 const KeyTiles kt = key_tiles(q0, BM, it.seq_len, a.K1, a.K2, BN);
                 const int n = key_tiles_count(kt);
@@ -132,6 +133,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int w = ring_take(&bars->ring, qi, lane);
             if (w < 0) break;
             const WorkItem it = a.items[w];
+            check_item(a, it, BM);
             const KeyTiles kt = key_tiles(it.tile * BM, BM, it.seq_len, a.K1, a.K2, BN);
             const int n = key_tiles_count(kt);
             const int kc0 = kc;
@@ -218,6 +220,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int w = ring_take(&bars->ring, qi, lane);
             if (w < 0) break;
             const WorkItem it = a.items[w];
+            check_item(a, it, BM);
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int q0 = it.tile * BM;
             const KeyTiles kt = key_tiles(q0, BM, L, a.K1, a.K2, BN);
@@ -276,6 +279,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->o_empty);
+            UH_CHECK(!qok || (int64_t)o + qp < a.T);
             if (qok) {
                 uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
                                                      (int64_t)(o + qp) * a.ld_out + h * DH + wg * 64);

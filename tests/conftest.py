@@ -10,6 +10,12 @@ for p in (ROOT, os.path.join(ROOT, "oracle")):
 
 
 def pytest_configure(config):
+    # UH_TEST_LIB=libuhstu_checked.so runs the suite against a variant build of the library
+    # (tools/build_variant.py; the checked build traps on any device-side range violation)
+    lib = os.environ.get("UH_TEST_LIB")
+    if lib:
+        from paper_2602_16986_b200 import uhstu as U
+        U.LIB_PATH = os.path.join(ROOT, "paper_2602_16986_b200", "lib", lib)
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; parity tests through the C-ABI")
     config.addinivalue_line("markers", "slow: long CPU/GPU runs (full-size configs)")
 

@@ -15,7 +15,7 @@ from attn_time import run
 run(B=16, rab=bool(int(sys.argv[1])) if len(sys.argv) > 1 else False, steps=1)
 t = buf.view(8, 1024).cpu().numpy()
 t0 = t[t > 0].min()
-names = ["S_issue", "PV_issue", "w4_wait_s", "w4_got_s", "w4_computed", "w4_arrived", "w8_got_s", "w8_arrived"]
+names = ["S_issue", "PV_issue", "w4_wait_s", "w4_got_s", "w4_computed", "w4_arrived", "w8_got_s", "ld_issue"]
 for j in range(400, 440):
     row = [(t[e, j] - t0) if t[e, j] > 0 else -1 for e in range(8)]
     print(j, " ".join(f"{n}={v:8d}" for n, v in zip(names, row)))
