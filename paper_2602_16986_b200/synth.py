@@ -172,3 +172,17 @@ def layer_inputs(cfg: Config, seed: Optional[int] = None, ids=None, lengths=None
     x = rows_normal(s, lengths, cfg.d, 1.0, 0x61, ids)
     dout = rows_normal(s, lengths, cfg.d, 1.0, 0x62, ids)
     return x, dout
+
+
+def mot_params(d: int, n_branches: int, seed: int):
+    """NEXT-4 fusion projection: W_f [K d, d] ~ N(0, 1/(K d)) (bf16-exact), b_f 0.1 N [d] (fp32)."""
+    r = _rng(seed, 0x307, n_branches)
+    f = np.float32
+    w = round_bf16(r.standard_normal((n_branches * d, d)).astype(f) / np.sqrt(n_branches * d))
+    return w, (0.1 * r.standard_normal(d)).astype(f)
+
+
+def mot_lengths(seed: int, B: int, lo: int, hi: int, branch: int) -> List[int]:
+    """Per-branch sequence lengths U[lo, hi] for the same B users (branch keys the stream)."""
+    r = _rng(seed, 0x3071, branch)
+    return [int(v) for v in r.integers(lo, hi + 1, size=B)]

@@ -24,8 +24,9 @@ def run(B=16, rab=True, K1=1024, K2=128, steps=10):
     dA = torch.randn(T, d, generator=g).to("cuda", torch.bfloat16)
     pos, ts = synth.rab_tables(cfg)
     t = synth.timestamps(cfg.seed, lengths)
-    attn = U.Attn(4, 128, 1.0, float(cfg.N), torch.from_numpy(pos).cuda() if rab else None,
-                  torch.from_numpy(ts).cuda() if rab else None, torch.from_numpy(t).cuda() if rab else None)
+    use_pos, use_ts = rab in (True, "pos"), rab in (True, "ts")   # rab = True / False / "pos" / "ts"
+    attn = U.Attn(4, 128, 1.0, float(cfg.N), torch.from_numpy(pos).cuda() if use_pos else None,
+                  torch.from_numpy(ts).cuda() if use_ts else None, torch.from_numpy(t).cuda() if use_ts else None)
     m = U.mask(K1, K2)
     A = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
     gb = torch.empty(T, 3 * d, dtype=torch.bfloat16, device="cuda")
@@ -63,6 +64,9 @@ def run(B=16, rab=True, K1=1024, K2=128, steps=10):
 
 
 if __name__ == "__main__":
+    if os.environ.get("ATTN_TIME_SPLIT"):   # rab cost split: position table only / time buckets only
+        run(rab="pos")
+        run(rab="ts")
     run(rab=True)
     run(rab=False)
     run(rab=False, K1=16383, K2=0, B=4)
