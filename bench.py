@@ -453,6 +453,96 @@ def run_inference(args, rank, world, local_rank):
             "e2e": None, "e2e_note": "inference inputs (x) stay resident; not measured for cfg5"}
 
 
+def run_mot(args, rank, world, local_rank):
+    """NEXT-4: one Mixture-of-Transducers training step per GPU — the paper's "10k
+    C-seq and 3k E-seq" row: per user a 10240-token consumption sequence through a
+    2-layer SLA transducer and a 3072-token engagement sequence through a 1-layer SLA transducer
+    (window 1024 + 128 global, rab on), the last 64 positions of each sequence are the candidates,
+    the fusion projects the concatenated [C, 2d] embeddings to d (readings R28-R30), then the
+    whole backward (fusion, both stacks; fp32 buckets all-reduced over NCCL for N > 1).
+    value = input tokens (both branches) of all GPUs per second."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_16986_b200 import dist as D
+    from paper_2602_16986_b200 import mot as GM
+    from paper_2602_16986_b200 import synth
+    from paper_2602_16986_b200 import uhstu as U
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    B, n_cand, d, H = args.mot_users, 64, 512, 4
+    spec = [("C-seq", 10240, 2), ("E-seq", 3072, 1)]
+    f = lambda a: torch.from_numpy(a).to(device)
+    bb = lambda a: torch.from_numpy(a).to(device, torch.bfloat16)
+    stacks, xs = [], []
+    for k, (name, L, n_layers) in enumerate(spec):
+        cfg = synth.Config(f"mot-{name}", [L] * B, H=H, dh=128, K1=1024, K2=128, N=L, seed=31 + 7 * rank + k)
+        m = U.mask(cfg.K1, cfg.K2)
+        pos, ts = synth.rab_tables(cfg)
+        t = f(synth.timestamps(cfg.seed, cfg.lengths))
+        layers = []
+        for li in range(n_layers):
+            pl = synth.layer_params(d, cfg.seed, layer=li)
+            prm = U.Params(f(pl["ln1_w"]), f(pl["ln1_b"]), bb(pl["w1"]), f(pl["ln2_w"]), f(pl["ln2_b"]),
+                           bb(pl["w2"]), f(pl["b1"]), f(pl["b2"]))
+            layers.append((prm, U.Attn(H, 128, 1.0, float(L), f(pos), f(ts), t)))
+        x = torch.randn(B * L, d, generator=torch.Generator(device=device).manual_seed(cfg.seed), device=device)
+        x = x.to(torch.bfloat16)
+        xs.append(x)
+        stacks.append(D.Stack(U.JaggedBatch(cfg.offsets(), device), m, layers, x))
+    W, bias = synth.mot_params(d, len(spec), 41)
+    mot = GM.MoT(stacks, n_cand, bb(W), f(bias))
+    dE = torch.randn(B * n_cand, d, generator=torch.Generator(device=device).manual_seed(43 + rank),
+                     device=device).to(torch.bfloat16)
+
+    def step():
+        mot.forward(xs)
+        _, handles = mot.backward(xs, dE)
+        for h in handles:
+            h.wait()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    l0 = U.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    launches = U.launch_count() - l0
+    clocks = sampler.stop() if sampler else None
+    if rank != 0:
+        return None
+    ms_step = ms / args.steps
+    tokens = B * sum(L for _, L, _ in spec) * world
+    return {"metric": "MoT training tokens/s (NEXT-4: 10k C-seq 2 SLA layers + 3k E-seq 1 SLA layer + fusion, fwd+bwd)",
+            "value": tokens / (ms_step / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"mot: {B} users per GPU; C-seq L=10240 x 2 layers, E-seq L=3072 x 1 layer, "
+                                   f"d=512, 4 heads x 128, SLA 1024 + 128 global, rab P=L, {n_cand} candidates "
+                                   f"per user, fusion [2d -> d]",
+                       "parallelism": f"dp{world}", "inputs_exceed_l2": True},
+            "gpu_launches": launches, "clocks": clocks,
+            "e2e": None, "e2e_note": "inputs stay resident; not measured for the MoT workload"}
+
+
 # ----------------------------------------------------------------------------- oracle arm
 def oracle_sample(cfg, L: int):
     """The oracle (as it stands) on one length-L sequence of the workload: layer fwd+bwd."""
@@ -513,10 +603,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg2", "cfg3", "cfg4", "cfg5", "mot"])
     ap.add_argument("--seq-len", type=int, default=16384, help="cfg5: sequence length (4096, 16384, 65536)")
     ap.add_argument("--tokens", type=int, default=4 * 1048576,
                     help="cfg5: tokens per GPU (0: as many as fill the GPU's free memory, BASELINE's cfg5)")
+    ap.add_argument("--mot-users", type=int, default=16, help="mot: users per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying a CUDA graph")
@@ -553,7 +644,8 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        line = (run_inference if args.config == "cfg5" else run_ours)(args, rank, world, local_rank)
+        run = {"cfg5": run_inference, "mot": run_mot}.get(args.config, run_ours)
+        line = run(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

@@ -147,6 +147,8 @@ uint64_t saved_fingerprint(const uh_jagged* jag, uh_mask m, const uh_layer_param
 
 }  // namespace
 
+uh_status uh::validate_jagged(const uh_jagged* j, bool need_device) { return check_jagged(j, need_device); }
+
 // =====================================================================================
 extern "C" {
 

@@ -36,6 +36,8 @@ uh_status make_tmap_u8(CUtensorMap* map, const void* ptr, uint64_t inner, uint64
 uh_status make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                         uint32_t box_inner, uint32_t box_outer);
 int num_sms();
+// the ABI's jagged-descriptor validation (abi.cu), shared by the other exported entry points
+uh_status validate_jagged(const uh_jagged* j, bool need_device);
 // every kernel launch of the library is counted (bench.py reports gpu_launches from it)
 void note_launch();
 

@@ -30,10 +30,10 @@ class GradBucket:
     """One flat fp32 buffer holding every parameter gradient; each view is 16-byte aligned
     (the C-ABI's alignment contract) and the whole bucket is one all-reduce."""
 
-    def __init__(self, shapes: Dict[str, Optional[Tuple[int, ...]]], device):
+    def __init__(self, shapes: Dict[str, Optional[Tuple[int, ...]]], device, names: Sequence[str] = GRAD_NAMES):
         n = 0
         self.offsets = {}
-        for k in GRAD_NAMES:
+        for k in names:
             s = shapes.get(k)
             if s is None:
                 continue
@@ -41,7 +41,7 @@ class GradBucket:
             self.offsets[k] = (n, s)
             n += (numel + 3) // 4 * 4
         self.flat = torch.zeros(max(n, 4), dtype=torch.float32, device=device)
-        self.views = {k: None for k in GRAD_NAMES}
+        self.views = {k: None for k in names}
         for k, (o, s) in self.offsets.items():
             self.views[k] = self.flat[o:o + int(np.prod(s))].view(s)
 
@@ -88,14 +88,18 @@ class Stack:
         self.ws_f = U._ws(U.layer_workspace_bytes(jag, m, prm0, att0, U.BF16, False), x.device)
         self.ws_b = U._ws(U.layer_workspace_bytes(jag, m, prm0, att0, U.BF16, True), x.device)
 
-    def step(self, x: torch.Tensor, dout: torch.Tensor, group=None):
-        """Forward through every layer, then the backward in reverse; layer l's gradient bucket
-        is all-reduced asynchronously right after its backward (NCCL overlaps layer l-1's
-        backward).  Returns the output, dx and the pending all-reduce handles."""
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """Every layer's forward (remat sets saved); returns the last layer's output."""
         h = x
         for (prm, attn), sv, out in zip(self.layers, self.saved, self.h):
             U.layer_fwd(self.jag, self.m, prm, attn, h, out=out, ws=self.ws_f, saved=sv)
             h = out
+        return h
+
+    def backward(self, x: torch.Tensor, dout: torch.Tensor, group=None):
+        """The backward in reverse after forward(x); layer l's gradient bucket is all-reduced
+        asynchronously right after its backward (NCCL overlaps layer l-1's backward).
+        Returns dx and the pending all-reduce handles."""
         handles = []
         g = dout
         for l in range(len(self.layers) - 1, -1, -1):
@@ -108,4 +112,11 @@ class Stack:
             if hd is not None:
                 handles.append(hd)
             g = dx
+        return g, handles
+
+    def step(self, x: torch.Tensor, dout: torch.Tensor, group=None):
+        """Forward through every layer, then the backward in reverse.  Returns the output, dx
+        and the pending all-reduce handles."""
+        h = self.forward(x)
+        g, handles = self.backward(x, dout, group)
         return h, g, handles

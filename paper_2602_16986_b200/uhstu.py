@@ -63,6 +63,11 @@ class LayerGrads(ctypes.Structure):
                 ("ln1_w", "ln1_b", "w1", "b1", "ln2_w", "ln2_b", "w2", "b2", "pos_bias", "time_bias")]
 
 
+class MotBranch(ctypes.Structure):
+    """uh_mot_branch (include/uhstu_mot.h)."""
+    _fields_ = [("jag", ctypes.POINTER(Jagged)), ("x", ctypes.c_void_p), ("ld", ctypes.c_int64)]
+
+
 class Fp8Weights(ctypes.Structure):
     """uh_fp8_weights (include/uhstu_fp8.h)."""
     _fields_ = [("w1t", ctypes.c_void_p), ("s1", ctypes.c_void_p), ("w2t", ctypes.c_void_p), ("s2", ctypes.c_void_p)]
@@ -127,6 +132,13 @@ def lib():
         L.uh_gather_rows.argtypes = [vp, i64, vp, i64, i64, i32, vp, i64, vp]
         for f in ("uh_lbsl_select", "uh_lbsl_subset", "uh_lbsl_rows", "uh_gather_rows"):
             getattr(L, f).restype = ctypes.c_int
+        # NEXT-4: MoT fusion (include/uhstu_mot.h)
+        L.uh_mot_workspace_bytes.argtypes = [i32, P(MotBranch), i32, i32, ctypes.c_int, ctypes.c_int, P(sz)]
+        L.uh_mot_fuse_fwd.argtypes = [i32, P(MotBranch), i32, i32, ctypes.c_int, vp, vp, vp, vp, sz, vp]
+        L.uh_mot_fuse_bwd.argtypes = [i32, P(MotBranch), i32, i32, ctypes.c_int, vp, vp, vp, vp, ctypes.c_int,
+                                      P(vp), P(i64), vp, sz, vp]
+        for f in ("uh_mot_workspace_bytes", "uh_mot_fuse_fwd", "uh_mot_fuse_bwd"):
+            getattr(L, f).restype = ctypes.c_int
         if L.uh_abi_version() != 1:
             raise RuntimeError("libuhstu ABI version mismatch")
         _lib = L
@@ -144,7 +156,7 @@ def exported_symbols() -> list:
             "uh_layer_bwd", "uh_jagged_gather", "uh_jagged_slice_latest", "uh_jagged_to_padded",
             "uh_padded_to_jagged", "uh_partition_lpt", "uh_ln_fwd_fp8", "uh_gated_norm_fwd_fp8",
             "uh_quant_weight_fp8", "uh_gemm_fp8", "uh_layer_fwd_fp8", "uh_lbsl_select", "uh_lbsl_subset",
-            "uh_lbsl_rows", "uh_gather_rows"]
+            "uh_lbsl_rows", "uh_gather_rows", "uh_mot_workspace_bytes", "uh_mot_fuse_fwd", "uh_mot_fuse_bwd"]
 
 
 def _check(st: int):
@@ -563,3 +575,49 @@ def gather_rows(rows_dev: torch.Tensor, x: torch.Tensor, out: Optional[torch.Ten
     _check(lib().uh_gather_rows(_ptr(rows_dev), n, _ptr(x), x.stride(0), x.shape[1], x.element_size(), _ptr(y),
                                 y.stride(0), _stream()))
     return y
+
+
+# ----------------------------------------------------------------------------- NEXT-4: MoT fusion
+def _mot_branches(jags: Sequence[JaggedBatch], xs: Sequence[torch.Tensor]):
+    if len(jags) != len(xs):
+        raise ValueError("one jagged batch per branch state")
+    arr = (MotBranch * len(xs))()
+    for i, (j, x) in enumerate(zip(jags, xs)):
+        arr[i] = MotBranch(ctypes.pointer(j.c), _ptr(x), x.stride(0))
+    return arr
+
+
+def mot_workspace_bytes(jags, xs, n_cand: int, backward: bool) -> int:
+    n = ctypes.c_size_t(0)
+    br = _mot_branches(jags, xs)
+    _check(lib().uh_mot_workspace_bytes(len(xs), br, int(n_cand), xs[0].shape[1], _dtype_code(xs[0]),
+                                        int(backward), ctypes.byref(n)))
+    return n.value
+
+
+def mot_fuse_fwd(jags, xs, n_cand: int, w_f: torch.Tensor, b_f: Optional[torch.Tensor], out=None, ws=None):
+    """E [B n_cand, d] = concat_k X_k[candidates] W_f + b_f (uh_mot_fuse_fwd)."""
+    d = xs[0].shape[1]
+    C = jags[0].B * n_cand
+    e = torch.empty(C, d, dtype=xs[0].dtype, device=xs[0].device) if out is None else out
+    if ws is None:
+        ws = _ws(mot_workspace_bytes(jags, xs, n_cand, False), xs[0].device)
+    _check(lib().uh_mot_fuse_fwd(len(xs), _mot_branches(jags, xs), int(n_cand), d, _dtype_code(xs[0]), _ptr(w_f),
+                                 _ptr(b_f), _ptr(e), _ptr(ws), ws.numel(), _stream()))
+    return e
+
+
+def mot_fuse_bwd(jags, xs, n_cand: int, w_f: torch.Tensor, de: torch.Tensor, dw_f: torch.Tensor,
+                 db_f: Optional[torch.Tensor] = None, accumulate: bool = False, dxs=None, ws=None):
+    """dW_f, db_f (fp32, overwritten or accumulated) and each branch's output gradient dX_k
+    (zero outside the candidate rows) -- uh_mot_fuse_bwd."""
+    d = xs[0].shape[1]
+    dxs = [torch.empty_like(x) for x in xs] if dxs is None else dxs
+    ptrs = (ctypes.c_void_p * len(xs))(*[_ptr(t) for t in dxs])
+    lds = (ctypes.c_int64 * len(xs))(*[t.stride(0) for t in dxs])
+    if ws is None:
+        ws = _ws(mot_workspace_bytes(jags, xs, n_cand, True), xs[0].device)
+    _check(lib().uh_mot_fuse_bwd(len(xs), _mot_branches(jags, xs), int(n_cand), d, _dtype_code(xs[0]), _ptr(w_f),
+                                 _ptr(de), _ptr(dw_f), _ptr(db_f), int(accumulate), ptrs, lds, _ptr(ws), ws.numel(),
+                                 _stream()))
+    return dxs

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     names = []
-    for h in ("uhstu.h", "uhstu_testing.h", "uhstu_fp8.h", "uhstu_lbsl.h"):
+    for h in ("uhstu.h", "uhstu_testing.h", "uhstu_fp8.h", "uhstu_lbsl.h", "uhstu_mot.h"):
         txt = open(os.path.join(ROOT, "include", h)).read()
         names += re.findall(r"UH_API\s+[\w\s\*]+?\b(uh_\w+)\s*\(", txt)
     return sorted(set(names))
@@ -189,3 +189,41 @@ def test_binding_rejects_mismatched_qkv_strides():
     with pytest.raises(ValueError):
         U._rows("dout", torch.zeros(64, 4).t())
     assert U._rows("q/k/v", q, q, q) == 64
+
+
+def test_mot_validation_before_launch():
+    """NEXT-4 (include/uhstu_mot.h): every argument check runs on the host before any launch."""
+    L = U.lib()
+
+    def branch_arr(jags, ld=64):
+        arr = (U.MotBranch * len(jags))()
+        for i, j in enumerate(jags):
+            j.c.offsets = ctypes.c_void_p(0x1000)        # never dereferenced: checks fail first
+            arr[i] = U.MotBranch(ctypes.pointer(j.c), ctypes.c_void_p(0x2000), ld)
+        return arr
+
+    def ws_status(jags, n_cand=2, d=64, dt=U.BF16, ld=64):
+        n = ctypes.c_size_t(0)
+        st = L.uh_mot_workspace_bytes(len(jags), branch_arr(jags, ld), n_cand, d, dt, 1, ctypes.byref(n))
+        return L.uh_status_string(st).decode(), n.value
+
+    a, b = _jag([0, 5, 9]), _jag([0, 3, 7])
+    st, n = ws_status([a, b])
+    assert st == "UH_OK" and n == 2 * ((2 * 2 * 2 * 64 * 2 + 255) // 256 * 256)
+    assert ws_status([a, _jag([0, 3, 7, 9])])[0] == "UH_ERR_DIM"          # different user counts (R29)
+    assert ws_status([a, _jag([0, 1, 7])])[0] == "UH_ERR_DIM"             # a sequence shorter than n_cand
+    assert ws_status([a, b], n_cand=0)[0] == "UH_ERR_DOMAIN"
+    assert ws_status([a] * 9)[0] == "UH_ERR_UNSUPPORTED"
+    assert ws_status([a, b], d=96)[0] == "UH_ERR_SHAPE"                   # bf16 needs d % 64 == 0
+    assert ws_status([a, b], ld=60)[0] == "UH_ERR_ALIGNMENT"
+    arr = branch_arr([a, b])
+    st = L.uh_mot_fuse_fwd(2, arr, 2, 64, U.BF16, None, None, ctypes.c_void_p(0x3000), None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_NULL"
+    st = L.uh_mot_fuse_fwd(2, arr, 2, 64, U.BF16, ctypes.c_void_p(0x3000), None, ctypes.c_void_p(0x3000), None, 0,
+                           None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_WORKSPACE"
+    dx = (ctypes.c_void_p * 2)(0x4000, 0x4008)
+    lds = (ctypes.c_int64 * 2)(64, 64)
+    st = L.uh_mot_fuse_bwd(2, arr, 2, 64, U.BF16, ctypes.c_void_p(0x3000), ctypes.c_void_p(0x3000),
+                           ctypes.c_void_p(0x3000), None, 0, dx, lds, None, 0, None)
+    assert L.uh_status_string(st).decode() == "UH_ERR_ALIGNMENT"
