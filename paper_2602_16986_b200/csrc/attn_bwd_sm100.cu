@@ -366,9 +366,10 @@ attn_bwd_fused_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_const
                     p2[c] = pack_bf16(pv.x, pv.y);
                     const uint64_t W = ffma2(H, ffma2(T, neg2, one2), one2);
                     const float2 dv = f2_unpack(fmul2(fmul2(f2_pack(dp[2 * c], dp[2 * c + 1]), A1), W));
-                    d2[c] = kok ? pack_bf16(dv.x, dv.y) : 0u;   // keys beyond L must not reach dQ
-                    dp[2 * c] = kok ? dv.x : 0.f;                // dp now holds the fp32 dS'
-                    dp[2 * c + 1] = kok ? dv.y : 0.f;
+                    // keys beyond L (must not reach dQ) arrive with h = dP = 0 (FLAG_M), so dS = 0
+                    d2[c] = pack_bf16(dv.x, dv.y);
+                    dp[2 * c] = dv.x;                             // dp now holds the fp32 dS'
+                    dp[2 * c + 1] = dv.y;
                 }
                 // P^T, dS^T -> TMEM over the consumed S^T / dP^T columns (A operands of dV, dK)
                 tmem_st16(tmem + lane_base + S_COL + sb * BN + 32 * wg, p2);

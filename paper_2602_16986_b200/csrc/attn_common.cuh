@@ -155,7 +155,8 @@ UH_HD int query_end(int k0, int rows, int L, int K1, int K2) {
 // Everything carries h = x/2 (x = alpha S + rab), the argument of tanh in
 // silu(x) = h + h tanh(h); tables are pre-halved.  Timestamps are 32-bit offsets
 // from the sequence's first timestamp (a sequence must span < 2^31 s).
-// Rows beyond L are "don't care" (never stored) and never raise a flag.
+// Rows beyond L are "don't care" in the forward (never stored) and never raise a flag there; in the
+// backward a key row beyond L raises FLAG_M, whose visibility mask zeroes its h and dP (dS = 0).
 //
 // Extended position table (built per call by rab_ext_k, attn.cu): two copies of
 // length Lt = max_len + 2 kPosOff, copy c holding e_c[i] = (pos[clamp(i + c - kPosOff,
@@ -284,7 +285,7 @@ UH_DEV Chunk k_chunk(const ChunkCtx& c, int kp, bool kok, int32_t tk, int qb, in
         r.hbias_o = hb + c.ts_h[bl];
         hb += c.ts_h[bf];
     }
-    r.flags = __reduce_or_sync(0xffffffffu, kok ? f : 0u);
+    r.flags = __reduce_or_sync(0xffffffffu, kok ? f : (unsigned)FLAG_M);   // keys beyond L: masked
     if (r.flags & FLAG_T1) {
         const int cnt = count_le<true>(tcol, thr);    // all lanes take part in the shuffles
         r.n = (r.b_other == r.b_base + 1) ? cnt : 32;
