@@ -10,17 +10,20 @@
 // work is O((K1 + K2) L) as the paper states.  No online-softmax state:
 // O accumulates in TMEM across all visited tiles with no rescale.
 //
-// Warp roles (384 threads, one CTA per SM, persistent over the LPT-ordered items):
+// Warp roles (512 threads, one CTA per SM, persistent over the LPT-ordered items):
 //   warp 0       TMA producer: Q tile once per item, (K,V) 64-key tiles through a 4-stage ring
 //   warp 1       MMA issuer:   Q smem -> TMEM once per item (tcgen05.cp); S[b] = Q K^T (TS: Q in
 //                TMEM, K from smem, N = 64); O += P V (TS: P over the consumed S columns, V MN-major)
 //   warp 2       TMEM allocator (512 columns: S0 | S1 | S2 at 0/64/128, O at 256, Q at 384)
-//   warps 4-11   epilogue: two warpgroups on alternate tiles; per 32-column chunk
-//                TMEM -> regs -> (alpha, rab, mask: warp-uniform fast path per chunk)
-//                -> silu via one tanh.approx -> bf16 P back into TMEM (tcgen05.st);
-//                at the end of an item O TMEM -> x 1/N -> bf16 A rows.
-// S is triple-buffered in TMEM: the MMA issues S(j) two tiles ahead of PV(j), so the
-// epilogue of one tile overlaps the MMAs of the next two.
+//   warps 4-15   epilogue: three warpgroups, tile j (S buffer j % 3) to warpgroup j % 3;
+//                per 32-column chunk TMEM -> regs -> (alpha, rab, mask: warp-uniform fast
+//                path per chunk) -> silu via one tanh.approx -> bf16 P back into TMEM
+//                (tcgen05.st); at the end of an item warpgroups 0 and 1 move O TMEM ->
+//                x 1/N -> bf16 A rows (64 columns each).
+// S is triple-buffered in TMEM: the MMA issues S(j) two tiles ahead of PV(j), so three
+// tiles' epilogues are in flight at once (one per warpgroup; the epilogue is latency-bound
+// with one warp per sub-partition and warpgroup: a third warpgroup took cfg3 from 1.284 to
+// 1.173 ms); 512 threads x 128 registers fill the register file.
 #include <climits>
 
 #include "attn_common.cuh"
@@ -38,7 +41,7 @@ constexpr int NS = 3;                   // S buffers in TMEM (64 columns each)
 constexpr int LAG = NS - 1;             // the MMA issues S(j) LAG tiles ahead of PV(j)
 constexpr int O_COL = 256;              // TMEM column of the O accumulator
 constexpr int Q_COL = 384;              // TMEM columns of Q (A operand of S = Q K^T), 64 packed columns
-constexpr int NUM_THREADS = 384;
+constexpr int NUM_THREADS = 512;
 constexpr int SMEM_BYTES = QT + STAGES * 2 * KT + 256 + 1024 + 512;
 
 struct __align__(8) FwdBars {
@@ -81,7 +84,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
         for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 4); }
         mbar_init(&bars->o_full, 1); mbar_init(&bars->o_empty, 8);
-        ring_init(&bars->ring, 9);   // MMA warp + 8 epilogue warps
+        ring_init(&bars->ring, 13);   // MMA warp + 12 epilogue warps
         fence_barrier_init();
     }
     stage_ts(a, ts_s);
@@ -210,7 +213,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp >= 4) {
         // ============================================================ epilogue
-        const int wg = (warp - 4) >> 2;      // warpgroup: handles the tiles of global parity wg
+        const int wg = (warp - 4) >> 2;      // warpgroup: handles the tiles j with j % 3 == wg
         const int wq = warp & 3;             // TMEM lane quarter
         const int r = wq * 32 + lane;        // row of the tile
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
@@ -229,10 +232,10 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const bool qok = qp < L;
             const ChunkCtx cx = make_ctx(a, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
-            // tiles alternate between the two warpgroups (global tile parity), so one group's
-            // MUFU-bound SiLU burst overlaps the other's TMEM traffic and bookkeeping
+            // tiles rotate over the three warpgroups (global tile index mod 3 = S buffer), so
+            // one group's SiLU burst overlaps the others' TMEM traffic, loads and bookkeeping
             for (int j = 0; j < n; ++j, ++sc) {
-                if ((sc & 1) != wg) continue;
+                if (sc % 3 != wg) continue;
                 const int sb = sc % NS;
                 const int k0 = key_tile_at(kt, j) * BN;
                 const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
@@ -269,7 +272,8 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
                 if (warp == 4 && lane == 0) TRACE(5 * 1024 + (sc & 1023));
             }
-            // ---- O epilogue: A = O / N
+            // ---- O epilogue: A = O / N (warpgroups 0 and 1, 64 columns each)
+            if (wg == 2) continue;
             mbar_wait_sleep(&bars->o_full, qi & 1);
             tc_fence_after();
             float ov[64];

@@ -40,6 +40,9 @@ def comp(cu):
     r = subprocess.run([B.NVCC, *B.ARCH, *flags, "-c", cu, "-o", obj], capture_output=True, text=True)
     if r.returncode:
         raise RuntimeError(r.stderr)
+    for ln in r.stderr.splitlines():          # -Xptxas -warn-spills
+        if "spill" in ln.lower() or "stack frame" in ln.lower():
+            print(os.path.basename(cu), ln.strip())
     return obj
 
 
