@@ -14,16 +14,17 @@
 //   warp 0       TMA producer: Q tile once per item, (K,V) 64-key tiles through a 5-stage ring
 //   warp 1       MMA issuer:   Q smem -> TMEM once per item (tcgen05.cp); S[b] = Q K^T (TS: Q in
 //                TMEM, K from smem, N = 64); O += P V (TS: P over the consumed S columns, V MN-major)
-//   warp 2       TMEM allocator (512 columns: S0 | S1 | S2 at 0/64/128, O at 256, Q at 384)
-//   warps 4-15   epilogue: three warpgroups, tile j (S buffer j % 3) to warpgroup j % 3;
+//   warp 2       TMEM allocator (512 columns: S0..S3 at 0/64/128/192, O at 256, Q at 384)
+//   warps 4-19   epilogue: four warpgroups, tile j (S buffer j % 4) to warpgroup j % 4;
 //                per 32-column chunk TMEM -> regs -> (alpha, rab, mask: warp-uniform fast
 //                path per chunk) -> silu via one tanh.approx -> bf16 P back into TMEM
-//                (tcgen05.st); at the end of an item warpgroups 0 and 1 move O TMEM ->
-//                x 1/N -> bf16 A rows (64 columns each).
-// S is triple-buffered in TMEM: the MMA issues S(j) two tiles ahead of PV(j), so three
-// tiles' epilogues are in flight at once (one per warpgroup; the epilogue is latency-bound
-// with one warp per sub-partition and warpgroup: a third warpgroup took cfg3 from 1.284 to
-// 1.173 ms); 512 threads x 128 registers fill the register file.
+//                (tcgen05.st); at the end of an item each warpgroup moves 32 O columns
+//                TMEM -> x 1/N -> bf16 A rows.
+// S has four TMEM buffers: the MMA issues S(j) three tiles ahead of PV(j), so four tiles'
+// epilogues are in flight at once (one per warpgroup).  The epilogue is latency-bound (a
+// warpgroup puts one warp on each sub-partition): cfg3 forward 1.284 ms with two
+// warpgroups, 1.173 with three, 1.111 with four (full causal with rab 1.601 -> 1.379 from
+// three to four; without rab four are 2-7% slower than three).
 #include <climits>
 
 #include "attn_common.cuh"
@@ -37,11 +38,16 @@ constexpr int QT = BM * DH * 2;          // 32 KB: Q tile, two 64-column swizzle
 constexpr int KT = BN * DH * 2;          // 16 KB: K (or V) tile, two 8 KB blocks
 constexpr int PT = BM * BN * 2;          // 16 KB: P tile, one block
 constexpr int STAGES = 5;               // (K,V) smem ring (4 -> 5: cfg3 equal, full causal 1.24 -> 1.14 ms)
-constexpr int NS = 3;                   // S buffers in TMEM (64 columns each)
+constexpr int NS = 4;                   // S buffers in TMEM (64 columns each)
 constexpr int LAG = NS - 1;             // the MMA issues S(j) LAG tiles ahead of PV(j)
 constexpr int O_COL = 256;              // TMEM column of the O accumulator
 constexpr int Q_COL = 384;              // TMEM columns of Q (A operand of S = Q K^T), 64 packed columns
-constexpr int NUM_THREADS = 512;
+constexpr int NUM_THREADS = 640;
+// registers per thread after setmaxnreg (640 threads start at 96): the control warpgroup gives
+// up 32, the four epilogue warpgroups take 8 more (an increase is served only from the CTA's
+// own releases: 128 x (96 - 64) >= 512 x (104 - 96))
+constexpr int REG_CTRL = 64, REG_EPI = 104;
+static_assert(128 * (96 - REG_CTRL) >= 512 * (REG_EPI - 96), "setmaxnreg: the epilogue increase must fit");
 constexpr int SMEM_BYTES = QT + STAGES * 2 * KT + 256 + 1024 + 512;
 
 struct __align__(8) FwdBars {
@@ -83,8 +89,8 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         mbar_init(&bars->q_full, 1); mbar_init(&bars->q_empty, 1);
         for (int i = 0; i < STAGES; ++i) { mbar_init(&bars->kv_full[i], 1); mbar_init(&bars->kv_empty[i], 1); }
         for (int i = 0; i < NS; ++i) { mbar_init(&bars->s_full[i], 1); mbar_init(&bars->p_full[i], 4); }
-        mbar_init(&bars->o_full, 1); mbar_init(&bars->o_empty, 8);
-        ring_init(&bars->ring, 13);   // MMA warp + 12 epilogue warps
+        mbar_init(&bars->o_full, 1); mbar_init(&bars->o_empty, 16);
+        ring_init(&bars->ring, 17);   // MMA warp + 16 epilogue warps
         fence_barrier_init();
     }
     stage_ts(a, ts_s);
@@ -95,6 +101,9 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem = bars->tmem;
 
+    if (warp < 4) {
+    // control warpgroup: TMA producer (warp 0), MMA issuer (warp 1), TMEM allocator (warp 2)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_CTRL));
     if (warp == 0) {
         // ============================================================ producer
         if (lane == 0) {
@@ -211,9 +220,11 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             kc += n; sc += n; pc += n;
         }
-    } else if (warp >= 4) {
+    }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_EPI));
         // ============================================================ epilogue
-        const int wg = (warp - 4) >> 2;      // warpgroup: handles the tiles j with j % 3 == wg
+        const int wg = (warp - 4) >> 2;      // warpgroup: handles the tiles j with j % 4 == wg
         const int wq = warp & 3;             // TMEM lane quarter
         const int r = wq * 32 + lane;        // row of the tile
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
@@ -232,10 +243,10 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const bool qok = qp < L;
             const ChunkCtx cx = make_ctx(a, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
-            // tiles rotate over the three warpgroups (global tile index mod 3 = S buffer), so
+            // tiles rotate over the four warpgroups (global tile index mod 4 = S buffer), so
             // one group's SiLU burst overlaps the others' TMEM traffic, loads and bookkeeping
             for (int j = 0; j < n; ++j, ++sc) {
-                if (sc % 3 != wg) continue;
+                if ((sc & 3) != wg) continue;
                 const int sb = sc % NS;
                 const int k0 = key_tile_at(kt, j) * BN;
                 const int32_t tc0 = col_time(cx, k0, lane), tc1 = col_time(cx, k0 + 32, lane);
@@ -272,13 +283,11 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
                 if (warp == 4 && lane == 0) TRACE(5 * 1024 + (sc & 1023));
             }
-            // ---- O epilogue: A = O / N (warpgroups 0 and 1, 64 columns each)
-            if (wg == 2) continue;
+            // ---- O epilogue: A = O / N (32 columns per warpgroup)
             mbar_wait_sleep(&bars->o_full, qi & 1);
             tc_fence_after();
-            float ov[64];
-            tmem_ld32(tmem + lane_base + O_COL + wg * 64, ov);
-            tmem_ld32(tmem + lane_base + O_COL + wg * 64 + 32, ov + 32);
+            float ov[32];
+            tmem_ld32(tmem + lane_base + O_COL + wg * 32, ov);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
@@ -286,10 +295,10 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             UH_CHECK(!qok || (int64_t)o + qp < a.T);
             if (qok) {
                 uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
-                                                     (int64_t)(o + qp) * a.ld_out + h * DH + wg * 64);
+                                                     (int64_t)(o + qp) * a.ld_out + h * DH + wg * 32);
                 const float sN = a.inv_n;
 #pragma unroll
-                for (int ch = 0; ch < 8; ++ch)
+                for (int ch = 0; ch < 4; ++ch)
                     op[ch] = make_uint4(pack_bf16(ov[ch * 8 + 0] * sN, ov[ch * 8 + 1] * sN),
                                         pack_bf16(ov[ch * 8 + 2] * sN, ov[ch * 8 + 3] * sN),
                                         pack_bf16(ov[ch * 8 + 4] * sN, ov[ch * 8 + 5] * sN),

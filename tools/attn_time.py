@@ -70,3 +70,5 @@ if __name__ == "__main__":
     run(rab=True)
     run(rab=False)
     run(rab=False, K1=16383, K2=0, B=4)
+    if os.environ.get("ATTN_TIME_CAUSAL_RAB"):   # full causal with rab (cfg2's mask at 16k)
+        run(rab=True, K1=16383, K2=0, B=4)
