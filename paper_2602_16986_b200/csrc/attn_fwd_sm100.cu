@@ -11,7 +11,7 @@
 // O accumulates in TMEM across all visited tiles with no rescale.
 //
 // Warp roles (512 threads, one CTA per SM, persistent over the LPT-ordered items):
-//   warp 0       TMA producer: Q tile once per item, (K,V) 64-key tiles through a 5-stage ring
+//   warp 0       TMA producer: Q tile once per item, (K,V) 64-key tiles through a 6-stage ring
 //   warp 1       MMA issuer:   Q smem -> TMEM once per item (tcgen05.cp); S[b] = Q K^T (TS: Q in
 //                TMEM, K from smem, N = 64); O += P V (TS: P over the consumed S columns, V MN-major)
 //   warp 2       TMEM allocator (512 columns: S0..S3 at 0/64/128/192, O at 256, Q at 384)
@@ -37,7 +37,9 @@ constexpr int BM = 128, BN = 64, DH = 128;
 constexpr int QT = BM * DH * 2;          // 32 KB: Q tile, two 64-column swizzled blocks of 16 KB
 constexpr int KT = BN * DH * 2;          // 16 KB: K (or V) tile, two 8 KB blocks
 constexpr int PT = BM * BN * 2;          // 16 KB: P tile, one block
-constexpr int STAGES = 5;               // (K,V) smem ring (4 -> 5: cfg3 equal, full causal 1.24 -> 1.14 ms)
+// (K,V) smem ring: the K of tile j loads once PV(j - STAGES) has completed; with four
+// epilogue warpgroups 5 -> 6 stages is cfg3-neutral and takes full causal from 1.23 to 1.07 ms
+constexpr int STAGES = 6;
 constexpr int NS = 4;                   // S buffers in TMEM (64 columns each)
 constexpr int LAG = NS - 1;             // the MMA issues S(j) LAG tiles ahead of PV(j)
 constexpr int O_COL = 256;              // TMEM column of the O accumulator
