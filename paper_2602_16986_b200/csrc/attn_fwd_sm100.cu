@@ -232,10 +232,12 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const uint32_t lane_base = (uint32_t)(wq * 32) << 16;
         const float ha = 0.5f * a.alpha;
         int sc = 0, qi = 0;
+        int w = ring_take(&bars->ring, 0, lane);
+        WorkItem itn{};
+        if (w >= 0) itn = a.items[w];
         for (;; ++qi) {
-            const int w = ring_take(&bars->ring, qi, lane);
             if (w < 0) break;
-            const WorkItem it = a.items[w];
+            const WorkItem it = itn;
             check_item(a, it, BM);
             const int L = it.seq_len, o = it.seq_start, h = it.head & 0xFFFF;
             const int q0 = it.tile * BM;
@@ -285,6 +287,25 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (lane == 0) mbar_arrive(&bars->p_full[sb]);
                 if (warp == 4 && lane == 0) TRACE(5 * 1024 + (sc & 1023));
             }
+            // the next item before this one's O epilogue (the o_full wait hides its loads)
+            const int wn = ring_take(&bars->ring, qi + 1, lane);
+            if (wn >= 0) {
+                itn = a.items[wn];
+                if (a.ts) {
+                    const int on = itn.seq_start, qn = itn.tile * BM;
+                    const KeyTiles ktn = key_tiles(qn, BM, itn.seq_len, a.K1, a.K2, BN);
+                    const int j0 = (wg - sc) & 3;   // this warpgroup's first tile of the next item
+                    const int64_t* tp = a.t + on;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + imin(qn + r, itn.seq_len - 1)));
+                    if (j0 < key_tiles_count(ktn)) {
+                        const int kb = key_tile_at(ktn, j0) * BN;
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + imin(kb + lane, itn.seq_len - 1)));
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + imin(kb + 32 + lane, itn.seq_len - 1)));
+                    }
+                }
+            }
+            w = wn;
             // ---- O epilogue: A = O / N (32 columns per warpgroup)
             mbar_wait_sleep(&bars->o_full, qi & 1);
             tc_fence_after();
