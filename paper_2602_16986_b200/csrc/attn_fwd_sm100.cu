@@ -14,14 +14,16 @@
 //   warp 0       TMA producer: Q tile once per item, (K,V) 64-key tiles through a 6-stage ring
 //   warp 1       MMA issuer:   Q smem -> TMEM once per item (tcgen05.cp); S[b] = Q K^T (TS: Q in
 //                TMEM, K from smem, N = 64); O += P V (TS: P over the consumed S columns, V MN-major)
-//   warp 2       TMEM allocator (512 columns: S0..S3 at 0/64/128/192, O at 256, Q at 384)
-//   warps 4-19   epilogue: four warpgroups, tile j (S buffer j % 4) to warpgroup j % 4;
+//   warp 2       TMEM allocator (512 columns: S0..S4 at 0/64/.../256, O at 320, Q at 448)
+//   warps 4-19   epilogue: four warpgroups, tile j to warpgroup j % 4 (S buffer j % 5);
 //                per 32-column chunk TMEM -> regs -> (alpha, rab, mask: warp-uniform fast
 //                path per chunk) -> silu via one tanh.approx -> bf16 P back into TMEM
 //                (tcgen05.st); at the end of an item each warpgroup moves 32 O columns
 //                TMEM -> x 1/N -> bf16 A rows.
-// S has four TMEM buffers: the MMA issues S(j) three tiles ahead of PV(j), so four tiles'
-// epilogues are in flight at once (one per warpgroup).  The epilogue is latency-bound (a
+// S has five TMEM buffers: the MMA issues S(j) four tiles ahead of PV(j), so four tiles'
+// epilogues are in flight at once (one per warpgroup) and each warpgroup's next S is already
+// issued while it finishes its current tile (five buffers over four warpgroups: cfg3 1.079 ->
+// 1.035 ms; full causal without rab 1.10 -> 1.22 ms, the longer S-to-PV lag holding K/V stages).  The epilogue is latency-bound (a
 // warpgroup puts one warp on each sub-partition): cfg3 forward 1.284 ms with two
 // warpgroups, 1.173 with three, 1.111 with four (full causal with rab 1.601 -> 1.379 from
 // three to four; without rab four are 2-7% slower than three).
@@ -40,10 +42,10 @@ constexpr int PT = BM * BN * 2;          // 16 KB: P tile, one block
 // (K,V) smem ring: the K of tile j loads once PV(j - STAGES) has completed; with four
 // epilogue warpgroups 5 -> 6 stages is cfg3-neutral and takes full causal from 1.23 to 1.07 ms
 constexpr int STAGES = 6;
-constexpr int NS = 4;                   // S buffers in TMEM (64 columns each)
+constexpr int NS = 5;                   // S buffers in TMEM (64 columns each)
 constexpr int LAG = NS - 1;             // the MMA issues S(j) LAG tiles ahead of PV(j)
-constexpr int O_COL = 256;              // TMEM column of the O accumulator
-constexpr int Q_COL = 384;              // TMEM columns of Q (A operand of S = Q K^T), 64 packed columns
+constexpr int O_COL = 320;              // TMEM column of the O accumulator
+constexpr int Q_COL = 448;              // TMEM columns of Q (A operand of S = Q K^T), 64 packed columns
 constexpr int NUM_THREADS = 640;
 // registers per thread after setmaxnreg (640 threads start at 96): the control warpgroup gives
 // up 32, the four epilogue warpgroups take 8 more (an increase is served only from the CTA's
@@ -247,8 +249,8 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const bool qok = qp < L;
             const ChunkCtx cx = make_ctx(a, ts_s, o, L);
             const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
-            // tiles rotate over the four warpgroups (global tile index mod 4 = S buffer), so
-            // one group's SiLU burst overlaps the others' TMEM traffic, loads and bookkeeping
+            // tiles rotate over the four warpgroups (global tile index mod 4), so one group's
+            // SiLU burst overlaps the others' TMEM traffic, loads and bookkeeping
             for (int j = 0; j < n; ++j, ++sc) {
                 if ((sc & 3) != wg) continue;
                 const int sb = sc % NS;
