@@ -10,6 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2602_16986_b200 import synth  # noqa: E402
 from paper_2602_16986_b200 import uhstu as U  # noqa: E402
+if os.environ.get("UH_LIB"):   # experiment builds (tools/build_exp.py)
+    U.LIB_PATH = os.path.join(ROOT, "paper_2602_16986_b200", "lib", os.environ["UH_LIB"])
 
 
 def t(fn, it=20):
