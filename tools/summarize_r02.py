@@ -110,6 +110,27 @@ def main():
             out.append(f"cfg5 L = {L} (`r02_cfg5_L{L}.json`): {d['value'] / 1e6:.2f} M input tokens/s, "
                        f"{d['config']['workload']}, HBM {d['config'].get('hbm_used_gb', 0):.0f} GB.")
     out.append("")
+    mf = os.path.join(P, "r02_mot_bench.json")
+    if os.path.exists(mf):
+        d = json.loads(open(mf).read().strip().splitlines()[-1])
+        out += ["## NEXT-4 Mixture of Transducers (`bench.py --config mot`): `r02_mot_bench.json`", "",
+                f"{d['value'] / 1e6:.1f} M input tokens/s at {d['ms_per_step']:.2f} ms per training step; "
+                f"{d['config']['workload']}.", ""]
+    af = os.path.join(P, "r02_attn_time.log")
+    if os.path.exists(af):
+        out += ["## Attention kernels alone (`tools/attn_time.py`, CUDA events): `r02_attn_time.log`", "", "```"]
+        out += [ln.strip() for ln in open(af) if ln.strip()] + ["```", ""]
+    ff = os.path.join(P, "r02_fp8_time.log")
+    if os.path.exists(ff):
+        out += ["## Projections, bf16 and FP8 (NEXT-2): `r02_fp8_time.log`, `r02_ncu_gemm_cfg3.json`", "", "```"]
+        out += [ln.rstrip() for ln in open(ff) if ln.strip() and not ln.startswith("#")] + ["```", ""]
+    gf = os.path.join(P, "r02_ncu_gemm_cfg3.json")
+    if os.path.exists(gf):
+        out += ["| GEMM | us | tensor pipe % | L1/smem % | issue % | SM GHz |", "|---|---|---|---|---|---|"]
+        for k in json.load(open(gf))["kernels"]:
+            out.append(f"| {k['gemm']} | {k['time_us']:.0f} | {k['tensor_pipe_active_pct']:.1f} | "
+                       f"{k['l1tex_throughput_pct']:.1f} | {k['issue_active_pct']:.1f} | {k['sm_clock_ghz']:.2f} |")
+        out.append("")
     cf = os.path.join(P, "r02_checked_tests.log")
     if os.path.exists(cf):
         last = [ln for ln in open(cf).read().splitlines() if ln.strip()][-1]
