@@ -236,7 +236,15 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         int sc = 0, qi = 0;
         int w = ring_take(&bars->ring, 0, lane);
         WorkItem itn{};
-        if (w >= 0) itn = a.items[w];
+        int64_t t0n = 0, tqn = 0;    // the next item's first timestamp and this row's (raw)
+        auto load_rowtimes = [&](const WorkItem& x) {
+            if (a.ts) {
+                t0n = __ldg(a.t + x.seq_start);
+                tqn = __ldg(a.t + x.seq_start + imin(x.tile * BM + r, x.seq_len - 1));
+            }
+        };
+        if (w >= 0) { itn = a.items[w]; load_rowtimes(itn); }
+        const float pos_far = a.pos ? 0.5f * __ldg(a.pos + a.P - 1) : 0.f;
         for (;; ++qi) {
             if (w < 0) break;
             const WorkItem it = itn;
@@ -247,8 +255,18 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int n = key_tiles_count(kt);
             const int qp = q0 + r;
             const bool qok = qp < L;
-            const ChunkCtx cx = make_ctx(a, ts_s, o, L);
-            const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
+            ChunkCtx cx;
+            cx.pe = a.pos ? a.pos_ext + kPosOff : nullptr;
+            cx.Lt = a.pos_ext_len;
+            cx.pos_far = pos_far;
+            cx.P = a.P;
+            cx.ts_h = a.ts ? ts_s : nullptr;
+            cx.NB = a.NB;
+            cx.t = a.t ? a.t + o : nullptr;
+            cx.t0 = a.ts ? t0n : 0;
+            cx.K1 = a.K1; cx.K2 = a.K2; cx.L = L;
+            cx.ha = 0.5f * a.alpha;
+            const int32_t tq = (a.ts && qok) ? rel32(tqn, cx.t0) : 0;
             // tiles rotate over the four warpgroups (global tile index mod 4), so one group's
             // SiLU burst overlaps the others' TMEM traffic, loads and bookkeeping
             for (int j = 0; j < n; ++j, ++sc) {
@@ -293,6 +311,7 @@ attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int wn = ring_take(&bars->ring, qi + 1, lane);
             if (wn >= 0) {
                 itn = a.items[wn];
+                load_rowtimes(itn);
                 if (a.ts) {
                     const int on = itn.seq_start, qn = itn.tile * BM;
                     const KeyTiles ktn = key_tiles(qn, BM, itn.seq_len, a.K1, a.K2, BN);
