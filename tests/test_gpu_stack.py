@@ -108,8 +108,11 @@ def test_cfg4_like_stack_per_layer_against_oracle():
         for k in ("w1", "w2", "ln1_w", "ln2_w", "b1"):
             e = rel_inf(to_np(grads[l][k]), ref_g[k])
             assert e <= 2e-2, (l, k, e)
-    # Stack.step runs the same calls in the same order: identical outputs and final dx
+    # Stack.step runs the same calls in the same order: the forward is bit-identical; the backward's
+    # fp32 reductions (dQ TMA reduce-adds in L2, split-K weight-gradient atomics) sum in an order
+    # that varies run to run, so dx may differ in the last bf16 place
     st = D.Stack(jag, m, list(zip(prms, [attn] * n_layers)), X)
     out_s, dx_s, _ = st.step(X, G)
     torch.cuda.synchronize()
-    assert torch.equal(out_s, hs[-1]) and torch.equal(dx_s, g)
+    assert torch.equal(out_s, hs[-1])
+    assert rel_inf(to_np(dx_s), to_np(g)) <= 1e-2
