@@ -4,18 +4,13 @@
 // forward of attn_fwd_sm100.cu (Eq. 3; SLA P:140-146; R5-R7):
 //     p = silu(s)/N, ds = dP * silu'(s)/N, dP = dA V^T, s = alpha Q K^T + rab
 //     dV = P^T dA,  dK = alpha dS^T Q,  dQ = alpha dS K,  d rab = scatter-sum of ds.
-// Default (fb::attn_bwd_fused_sm100, one key-major pass): per 128-key tile (K, V resident in
+// One kernel, fb::attn_bwd_fused_sm100 (a key-major pass): per 128-key tile (K, V resident in
 // shared memory), over the 64-query steps that see it: S^T = K Q^T and dP^T = V dA^T (SS);
-// P^T, dS^T (bf16) over the consumed TMEM columns; dV += P^T dA, dK += dS^T Q (TS);
-// dQ^T = K^T dS^T (SS, dS^T also in shared memory) over the consumed S^T columns, read by
-// a fourth warpgroup and TMA-added into an fp32 [T, H dh] accumulator, which dq_finish_k
-// scales and gates into dQ.  That warpgroup also reduces d pos_bias / d time_bias.
-// UH_ATTN_BWD=split selects the earlier two-kernel path (no fp32 accumulator):
-//   dq kernel  (query-major): per 128-query tile, over its visible 64-key tiles:
-//              S = Q K^T, dP = dA V^T with Q, dA as TMEM A operands (tcgen05.cp once per
-//              item); dS (bf16) written over the consumed S columns; dQ += dS K (dS as
-//              TMEM A operand).  Also reduces d pos_bias / d time_bias.
-//   dkv kernel (key-major):   the default kernel's dV / dK part, K/V double-buffered.
+// the P/dS warpgroups (warps 4-11) write P^T, dS^T (bf16) over the consumed TMEM columns and
+// dS^T to shared memory, and sum d time_bias; dV += P^T dA, dK += dS^T Q (TS);
+// dQ^T = K^T dS^T (SS) over the consumed S^T columns, read by the two dQ warpgroups (warps
+// 12-19) and TMA-added into an fp32 [T, H dh] accumulator, which dq_finish_k scales and
+// gates into dQ; the dQ warpgroups also sum d pos_bias from the dS^T tile.
 // TMEM buffers are reused in tensor-pipe order (an MMA issued after another by the same
 // thread executes after it).
 // Gradients are multiplied by optional gates (silu'(h), the layer's fused
