@@ -6,7 +6,7 @@ PATCHES = [
     ("attn_fwd_sm100.cu", "                if (warp == 8 && lane == 0) TRACE(6 * 1024 + (sc & 1023));\n", ""),
     ("attn_fwd_sm100.cu", """            if (lane == 0) mbar_arrive(&bars->o_empty);""", """            if (lane == 0) mbar_arrive(&bars->o_empty);
             if (warp == 4 && lane == 0) TRACE(6 * 1024 + (sc & 1023));"""),
-    ("attn_fwd_sm100.cu", """            const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;""",
-     """            const int32_t tq = (a.ts && qok) ? rel32(__ldg(a.t + o + qp), cx.t0) : 0;
+    ("attn_fwd_sm100.cu", """            const int32_t tq = (a.ts && qok) ? rel32(tqn, cx.t0) : 0;""",
+     """            const int32_t tq = (a.ts && qok) ? rel32(tqn, cx.t0) : 0;
             if (warp == 4 && lane == 0) TRACE(7 * 1024 + ((sc + (tq & 0) + (int)(cx.pos_far * 0.f)) & 1023));"""),
 ]
