@@ -69,6 +69,9 @@ def main():
         for r in rows[1:]:
             nm = r[ki]
             lab = label(nm)[0]
+            if lab == "?":   # not one of the library's kernels (torch fills / copies of the harness)
+                lab = "other: `" + re.sub(r"\(.*", "", nm).replace("void ", "")[:48] + "`"
+
             agg.setdefault(lab, []).append(float(r[vi].replace(",", "")) / 1e3)
         out += ["## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, cold-cache, serialised): "
                 "`r02_bench_launches.csv`", "",
