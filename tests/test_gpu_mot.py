@@ -143,3 +143,30 @@ def test_mot_step_matches_oracle():
             for name in ("w1", "w2", "ln1_w", "b1"):
                 e = rel_inf(to_np(views[name]), g_ref[name])
                 assert e <= TOLB, (k, l, name, e)
+
+
+@pytest.mark.parametrize("K,B,n_cand", [(8, 3, 2), (1, 1, 7)])
+def test_fusion_edge_shapes(K, B, n_cand):
+    """The branch limit (8), a single branch, a single user and n_cand equal to a whole sequence."""
+    d = 128
+    r = np.random.default_rng(K * 10 + B)
+    lens = [[n_cand] + synth.mot_lengths(9, B - 1, n_cand, 40, k) for k in range(K)]
+    offs = [_offsets(l) for l in lens]
+    xs = [synth.round_bf16(r.standard_normal((int(o[-1]), d)).astype(np.float32)) for o in offs]
+    W, bias = synth.mot_params(d, K, 13)
+    dE = synth.round_bf16(r.standard_normal((B * n_cand, d)).astype(np.float32))
+    brs = [M.Branch(x=x, offsets=o, layers=[]) for x, o in zip(xs, offs)]
+    E_ref, cache = M.mot_forward(brs, n_cand, W, bias)
+    dxs_ref, _, dW_ref, db_ref = M.mot_backward(dE, brs, n_cand, W, bias, cache=cache)
+    jags = [U.JaggedBatch(o) for o in offs]
+    X = [to_dev(x, U.BF16) for x in xs]
+    Wd, bd = to_dev(W, U.BF16), torch.from_numpy(bias).cuda()
+    E = U.mot_fuse_fwd(jags, X, n_cand, Wd, bd)
+    dW = torch.empty(K * d, d, device="cuda")
+    db = torch.empty(d, device="cuda")
+    dxs = U.mot_fuse_bwd(jags, X, n_cand, Wd, to_dev(dE, U.BF16), dW, db)
+    torch.cuda.synchronize()
+    assert rel_inf(to_np(E), E_ref) <= 2e-2
+    assert rel_inf(to_np(dW), dW_ref) <= 2e-2 and rel_inf(to_np(db), db_ref) <= 2e-2
+    for k in range(K):
+        assert rel_inf(to_np(dxs[k]), dxs_ref[k]) <= 2e-2

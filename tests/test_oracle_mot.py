@@ -143,3 +143,18 @@ def test_backward_finite_differences():
         arr = spec.pos_w if name == "pos_w" else getattr(prm, name)
         g = fd(L, arr, idx)
         assert abs(g - grads[k][li][name][idx]) < 1e-6 * max(1.0, abs(g)), (k, li, name, g)
+
+
+def test_every_row_a_candidate_is_a_plain_projection():
+    """n_cand = L for every sequence: the fusion is the row-aligned concatenation of the branch
+    outputs times W_f (checked against an explicit matmul of the stacked outputs)."""
+    a = _branch(5, (4, 6), 1)
+    b = _branch(6, (4, 6), 2, K1=O.FULL, K2=0)
+    W, bias = synth.mot_params(6, 2, 8)
+    W, bias = np.asarray(W, np.float64), np.asarray(bias, np.float64)
+    E, _ = M.mot_forward([a, b], 4, W, bias)          # n_cand = 4 = shortest length; rows 2..5 of user 1
+    oa, _ = M.branch_forward(a)
+    ob, _ = M.branch_forward(b)
+    rows = np.r_[0:4, 6:10]
+    want = np.concatenate([oa[rows], ob[rows]], axis=1) @ W + bias
+    assert np.max(np.abs(E - want)) < 1e-12
