@@ -197,6 +197,27 @@ def test_attn_position_table_longer_than_sequences(K1, K2):
 
 
 # ----------------------------------------------------------------------------- layer
+def test_attn_row_strides_off_32_bytes():
+    """Output / gradient row strides that are 16- but not 32-byte multiples (width + 8 elements):
+    the per-thread O, dV, dK rows then take the 16-byte store path instead of the 32-byte one."""
+    case = AttnCase([70, 300, 129], H=2, dh=128, K1=64, K2=8, N=300.0, P=400, seed=3)
+    jag = case.jag()
+    w = case.cfg.H * case.cfg.dh
+    _, q, k, v = case.fused_qkv(U.BF16)
+    out = torch.empty(q.shape[0], w + 8, dtype=torch.bfloat16, device="cuda")[:, :w]
+    A = U.attn_fwd(jag, case.mask(), case.desc(), q, k, v, out=out)
+    g = torch.empty(q.shape[0], 3 * w + 8, dtype=torch.bfloat16, device="cuda")
+    dq, dk, dv = g[:, :w], g[:, w:2 * w], g[:, 2 * w:3 * w]
+    U.attn_bwd(jag, case.mask(), case.desc(), q, k, v, to_dev(case.dA, U.BF16), dq=dq, dk=dk, dv=dv)
+    torch.cuda.synchronize()
+    assert out.stride(0) * 2 % 32 and g.stride(0) * 2 % 32
+    assert rel_inf(to_np(A), oracle_fwd(case)) <= TOL[U.BF16]
+    ref = oracle_bwd(case)
+    for n, got, r in zip(("dQ", "dK", "dV"), (dq, dk, dv), ref[:3]):
+        e = rel_inf(to_np(got), r)
+        assert e <= TOL[U.BF16], (n, e)
+
+
 def layer_case(cfg, dtype, biases=True):
     p = synth.layer_params(cfg.d, cfg.seed, biases=biases)
     x, dout = synth.layer_inputs(cfg)
