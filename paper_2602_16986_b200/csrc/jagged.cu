@@ -17,8 +17,9 @@ struct SegBatch { Seg s[kSegs]; int n; };
 // copy `len` rows per segment with VT-wide vectors (uint4: row bytes and both strides multiples of
 // 16; uint2: multiples of 8, e.g. int64 timestamps or an odd 8-byte stride)
 template <typename VT>
-__global__ void __launch_bounds__(256) copy_rows_k(SegBatch b, const uint8_t* __restrict__ x, int64_t ldx_bytes,
-                                                   uint8_t* __restrict__ y, int64_t ldy_bytes, int64_t row_bytes) {
+__global__ void __launch_bounds__(256) copy_rows_k(const __grid_constant__ SegBatch b, const uint8_t* __restrict__ x,
+                                                   int64_t ldx_bytes, uint8_t* __restrict__ y, int64_t ldy_bytes,
+                                                   int64_t row_bytes) {
     const int seg = blockIdx.y;
     if (seg >= b.n) return;
     const Seg s = b.s[seg];
@@ -38,8 +39,8 @@ __global__ void __launch_bounds__(256) copy_rows_k(SegBatch b, const uint8_t* __
 }
 
 template <typename VT>
-__global__ void __launch_bounds__(256) zero_rows_k(SegBatch b, uint8_t* __restrict__ y, int64_t ldy_bytes,
-                                                   int64_t row_bytes) {
+__global__ void __launch_bounds__(256) zero_rows_k(const __grid_constant__ SegBatch b, uint8_t* __restrict__ y,
+                                                   int64_t ldy_bytes, int64_t row_bytes) {
     const int seg = blockIdx.y;
     if (seg >= b.n) return;
     const Seg s = b.s[seg];

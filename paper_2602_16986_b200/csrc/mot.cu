@@ -35,8 +35,8 @@ __device__ __forceinline__ int64_t cand_row(const int32_t* off, int64_t c, int n
 
 // SCATTER = false: Z[c, k row_bytes ...] = X_k[cand_row];  true: X_k[cand_row] = Z[c, k row_bytes ...]
 template <bool SCATTER>
-__global__ void __launch_bounds__(256) mot_rows_k(MotRows br, int64_t C, int n_cand, int64_t row_bytes,
-                                                  uint8_t* __restrict__ z, int64_t ldz_bytes) {
+__global__ void __launch_bounds__(256) mot_rows_k(const __grid_constant__ MotRows br, int64_t C, int n_cand,
+                                                  int64_t row_bytes, uint8_t* __restrict__ z, int64_t ldz_bytes) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * 8, n = C * br.n, nvec = row_bytes / 16;
     for (int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); i < n; i += warps) {
